@@ -1,0 +1,42 @@
+"""Shared fixtures.  Tests needing a B200 are marked `@pytest.mark.gpu`."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers",
+                            "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def golden(name):
+    """Load one fixture written by tests/golden/make_golden.py."""
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+
+
+def golden_cloud(fx, prefix=""):
+    from oracle import Cloud
+    return Cloud(*(fx[prefix + k].astype(np.float64) for k in
+                   ("positions", "log_scales", "rotations", "raw_opacities",
+                    "mlp_weights")),
+                 mlp_dims=tuple(int(v) for v in fx[prefix + "mlp_dims"]))
+
+
+def golden_dL(fx):
+    h, w = int(fx["h"]), int(fx["w"])
+    U = np.random.default_rng(int(fx["dL_seed"])).normal(size=(h, w, 2))
+    assert np.isclose(U.sum(), float(fx["dL_sum"]), rtol=0, atol=1e-9)
+    return U
+
+
+@pytest.fixture
+def origin():
+    return np.zeros(3), np.eye(3)
