@@ -1,0 +1,177 @@
+// Shared definitions for the GSpaRC B200 kernels (sm_100a).
+//
+// Layout conventions:
+//   cloud, source order:  positions f64 (N,3) | log_scales f64 (N,3) |
+//                         rotations f64 (N,4) (w,x,y,z) | raw_opacities f64 (N)
+//                         mlp_weights f32 (N,P), row = W1(h*i)|b1(h)|W2(o*h)|b2(o)
+//                         (reference scene.py:46-103, mlp.py:6-7)
+//   per-Gaussian records, source order (written by k_preprocess):
+//     key   u64   radial-depth bit pattern (culled -> ~0)
+//     rec32 2x float4 {mx,my,ca,cb} {cc,opac,theta,phi}   (f32 raster record)
+//     rec64 8x f64    {mx,my,ca,cb,cc,opac,theta,phi}     (f64 raster record)
+//     rect  int4      {y0 | y1<<16, a0 | a1<<16, b0 | b1<<16, npairs}
+//   tile lists: tile_start[T+1] (exclusive scan) and pairs[] u64
+//     = (coarse_depth32 << 32) | source_index, sorted per tile.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gsparc_b200.h"
+
+namespace gs {
+
+constexpr int TILE = 16;
+constexpr int TILE_PX = TILE * TILE;
+constexpr double NEAR_PLANE = 0.05;      // geometry.py:27
+constexpr double FAR_PLANE = 1000.0;     // geometry.py:28
+constexpr double COV2D_REG = 0.3;        // geometry.py:19
+constexpr double FOOTPRINT_SIGMA = 3.3290429691304455;  // geometry.py:25
+constexpr double ALPHA_MAX = 0.99;       // rasterizer.py:33
+constexpr double ALPHA_MIN = 1.0 / 255.0;  // rasterizer.py:34
+constexpr float ALPHA_MAX_F = 0.99f;
+constexpr float ALPHA_MIN_F = (float)(1.0 / 255.0);  // 0x3b808081
+
+// Bit pattern of NEAR_PLANE: subtracting it keeps kept-depth keys < 2^56,
+// so (key - base) >> 24 is a monotone 32-bit coarse key (SURVEY 7 hard 1).
+constexpr uint64_t DEPTH_KEY_BASE = 0x3FA999999999999AULL;  // bits(0.05)
+constexpr int COARSE_SHIFT = 24;
+
+struct Pose {
+  double rx[3];
+  double W[9];
+};
+
+// Host-computed constants so device and numpy agree bit for bit.
+struct GeoConst {
+  double ca, ce;          // w/(2 pi), 2h/pi            (geometry.py:140-141)
+  double half_w_over_pi;  // not used for math order; kept for clarity
+  double pole_lim;        // deg2rad(89)                 (geometry.py:103)
+  double cos2_lim;        // cos(lim)**2                 (geometry.py:131)
+  double cos_lim, sin_lim;
+  double inv_pi;          // unused; numpy divides by pi, we do too
+  double pi;
+  int w, h, ntx, nty;
+};
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// numpy float remainder (npy_divmod): fmod, then shift into the sign of b.
+template <typename R>
+__device__ __forceinline__ R py_mod(R a, R b);
+
+template <>
+__device__ __forceinline__ float py_mod<float>(float a, float b) {
+  float m = fmodf(a, b);
+  if (m != 0.0f) {
+    if ((b < 0.0f) != (m < 0.0f)) m = __fadd_rn(m, b);
+  } else {
+    m = copysignf(0.0f, b);
+  }
+  return m;
+}
+
+template <>
+__device__ __forceinline__ double py_mod<double>(double a, double b) {
+  double m = fmod(a, b);
+  if (m != 0.0) {
+    if ((b < 0.0) != (m < 0.0)) m = __dadd_rn(m, b);
+  } else {
+    m = copysign(0.0, b);
+  }
+  return m;
+}
+
+// Exact arithmetic helpers that forbid FMA contraction so the operation
+// order of the numpy reference is reproduced.
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float exp_r(float x) { return expf(x); }
+__device__ __forceinline__ double exp_r(double x) { return exp(x); }
+
+// Per-pixel alpha exactly in the order of rasterizer.py:177-183.
+// Returns alpha (0 when below ALPHA_MIN) and optionally raw/g/dx/dy.
+template <typename R>
+struct AlphaOut {
+  R alpha, raw, g, dx, dy;
+};
+
+template <typename R>
+__device__ __forceinline__ AlphaOut<R> pixel_alpha(R pcx, R pcy, R mx, R my, R ca,
+                                                  R cb, R cc, R op, R w, R half_w) {
+  AlphaOut<R> o;
+  R t = add(sub(pcx, mx), half_w);
+  // fast exact remainder for t in [-w, 2w); general fallback otherwise
+  R m;
+  if (t >= R(0) && t < w) {
+    m = t;
+  } else if (t >= w && t < R(2) * w) {
+    m = sub(t, w);  // exact (Sterbenz)
+  } else if (t < R(0) && t > -w) {
+    m = add(t, w);  // numpy: fmod(t,w)=t, then t+w rounded
+  } else {
+    m = py_mod<R>(t, w);
+  }
+  o.dx = sub(m, half_w);
+  o.dy = sub(pcy, my);
+  R q = add(add(mul(mul(ca, o.dx), o.dx), mul(mul(mul(R(2), cb), o.dx), o.dy)),
+            mul(mul(cc, o.dy), o.dy));
+  o.g = exp_r(mul(R(-0.5), q));
+  o.raw = mul(op, o.g);
+  R amax = sizeof(R) == 4 ? R(ALPHA_MAX_F) : R(ALPHA_MAX);
+  R amin = sizeof(R) == 4 ? R(ALPHA_MIN_F) : R(ALPHA_MIN);
+  R a = o.raw < amax ? o.raw : amax;  // np.minimum (NaN-free inputs)
+  o.alpha = (a < amin) ? R(0) : a;
+  return o;
+}
+
+template <typename R>
+struct Rec {  // raster record in the raster precision
+  R mx, my, ca, cb, cc, op;
+};
+
+__device__ __forceinline__ Rec<float> load_rec(const float4* rec32, const double*, uint32_t i) {
+  float4 a = __ldg(rec32 + 2 * i);
+  float4 b = __ldg(rec32 + 2 * i + 1);
+  return {a.x, a.y, a.z, a.w, b.x, b.y};
+}
+__device__ __forceinline__ Rec<double> load_rec(const float4*, const double* rec64, uint32_t i,
+                                                int /*tag*/) {
+  const double* p = rec64 + 8 * (size_t)i;
+  return {p[0], p[1], p[2], p[3], p[4], p[5]};
+}
+
+template <typename R>
+__device__ __forceinline__ Rec<R> load_rec_t(const float4* rec32, const double* rec64, uint32_t i) {
+  if constexpr (sizeof(R) == 4) {
+    return load_rec(rec32, rec64, i);
+  } else {
+    return load_rec(rec32, rec64, i, 0);
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- host side
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+}  // namespace gs
+
+#define GS_TRY(expr)                       \
+  do {                                     \
+    int _rc = (expr);                      \
+    if (_rc != GSPARC_OK) return _rc;      \
+  } while (0)

@@ -1,0 +1,260 @@
+// K7: training loss on device.  Replaces image.magnitude /
+// magnitude_backward (image.py:46-61) and optimize.combined_loss with the
+// exact SSIM adjoint (optimize.py:67-188):
+//   loss_b = (1-lam) mean|p-g| + lam (1 - mean_c SSIM_c)
+// SSIM: 11-tap Gaussian window (sigma 1.5), separable, scipy 'reflect'
+// (half-sample symmetric) padding; gradient through the adjoint filter
+// (zero-padded correlation folded back at the borders, optimize.py:97-115).
+// f64 throughout (variance terms cancel).  Pipeline, one thread per pixel:
+//   h-blur of (x, y, xx, yy, xy) -> v-blur + SSIM map + adjoint seeds
+//   -> adjoint v -> adjoint h + L1 term + magnitude chain -> dimg.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gs {
+
+// optimize.py:81-87: x = arange(11) - 5; w = exp(-(x/1.5)^2/2) / sum
+static void make_window(double* w) {
+  double s = 0.0;
+  for (int t = 0; t < 11; ++t) {
+    double x = (double)t - 5.0;
+    w[t] = exp(-0.5 * ((x / 1.5) * (x / 1.5)));
+    s += w[t];
+  }
+  for (int t = 0; t < 11; ++t) w[t] /= s;
+}
+
+struct LossArgs {
+  double win[11];
+  const float* img;
+  const float* gt;
+  float* dimg;
+  double* H5;    // [5][NI][S][h][w]
+  double* G3;    // [3][NI][S][h][w]
+  double* A3;    // [3][NI][S][h][w]
+  double* sums;  // [NI][S+2]: ssim_c sums..., l1 sum, sq sum
+  double* stats; // [NI][4]
+  int NI, S, C, h, w, sup;
+  double lam;
+};
+
+__device__ __forceinline__ int refl(int j, int n) {
+  if (j < 0) return -j - 1;
+  if (j >= n) return 2 * n - 1 - j;
+  return j;
+}
+
+__device__ __forceinline__ double pred_at(const LossArgs& A, int b, int s, int r, int c) {
+  const float* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+  if (A.sup == 0) return hypot((double)z[0], (double)z[1]);
+  return (double)z[s];
+}
+__device__ __forceinline__ double gt_at(const LossArgs& A, int b, int s, int r, int c) {
+  return (double)A.gt[(((int64_t)b * A.h + r) * A.w + c) * A.S + s];
+}
+
+__global__ void k_loss_h(LossArgs A) {
+  const int64_t plane = (int64_t)A.h * A.w;
+  const int64_t tot = (int64_t)A.NI * A.S * plane;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
+  const int64_t bs = e / plane;
+  const int s = (int)(bs % A.S), b = (int)(bs / A.S);
+  double a[5] = {0, 0, 0, 0, 0};
+  for (int t = 0; t < 11; ++t) {
+    const int cc = refl(c + t - 5, A.w);
+    const double x = pred_at(A, b, s, r, cc), y = gt_at(A, b, s, r, cc);
+    const double wt = A.win[t];
+    a[0] += wt * x;
+    a[1] += wt * y;
+    a[2] += wt * (x * x);
+    a[3] += wt * (y * y);
+    a[4] += wt * (x * y);
+  }
+  for (int k = 0; k < 5; ++k) A.H5[k * tot + e] = a[k];
+}
+
+__global__ void k_loss_v(LossArgs A) {
+  const int64_t plane = (int64_t)A.h * A.w;
+  const int64_t tot = (int64_t)A.NI * A.S * plane;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double ssim_v = 0.0, l1_v = 0.0, sq_v = 0.0;
+  int b = 0, s = 0;
+  if (e < tot) {
+    const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
+    const int64_t bs = e / plane;
+    s = (int)(bs % A.S);
+    b = (int)(bs / A.S);
+    const int64_t rowbase = bs * plane;
+    double m[5] = {0, 0, 0, 0, 0};
+    for (int t = 0; t < 11; ++t) {
+      const int rr = refl(r + t - 5, A.h);
+      const double wt = A.win[t];
+      for (int k = 0; k < 5; ++k) m[k] += wt * A.H5[k * tot + rowbase + (int64_t)rr * A.w + c];
+    }
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    const double mx = m[0], my = m[1];
+    const double vx = m[2] - mx * mx, vy = m[3] - my * my, vxy = m[4] - mx * my;
+    const double a1 = 2 * mx * my + c1, a2 = 2 * vxy + c2;
+    const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
+    const double sv = (a1 * a2) / (b1 * b2);
+    const double da1 = a2 / (b1 * b2), da2 = a1 / (b1 * b2);
+    const double db1 = -sv / b1, db2 = -sv / b2;
+    A.G3[e] = 2 * my * da1 - 2 * my * da2 + 2 * mx * db1 - 2 * mx * db2;
+    A.G3[tot + e] = db2;
+    A.G3[2 * tot + e] = 2 * da2;
+    ssim_v = sv;
+    const double x = pred_at(A, b, s, r, c), y = gt_at(A, b, s, r, c);
+    l1_v = fabs(x - y);
+    sq_v = (x - y) * (x - y);
+  }
+  // per-(image, channel) sums: warp-reduce when the warp lies in one plane
+  const unsigned full = 0xffffffffu;
+  const int key = (e < tot) ? (b * A.S + s) : -1;
+  const int leader_key = __shfl_sync(full, key, 0);
+  const bool uniform = __all_sync(full, key == leader_key);
+  if (uniform) {
+    ssim_v = warp_sum(ssim_v);
+    l1_v = warp_sum(l1_v);
+    sq_v = warp_sum(sq_v);
+    if ((threadIdx.x & 31) == 0 && key >= 0) {
+      double* sm = A.sums + (int64_t)b * (A.S + 2);
+      atomicAdd(sm + s, ssim_v);
+      atomicAdd(sm + A.S, l1_v);
+      atomicAdd(sm + A.S + 1, sq_v);
+    }
+  } else if (key >= 0) {
+    double* sm = A.sums + (int64_t)b * (A.S + 2);
+    atomicAdd(sm + s, ssim_v);
+    atomicAdd(sm + A.S, l1_v);
+    atomicAdd(sm + A.S + 1, sq_v);
+  }
+}
+
+// adjoint along rows: out[r] = G(r) + [r<5] G(-r-1) + [r>=h-5] G(2h-1-r),
+// G(j) = sum_t w[t] g[j+t-5] (g = 0 outside [0,h))
+__device__ __forceinline__ double adj_line(const LossArgs& A, const double* g, int stride, int n,
+                                          int i) {
+  auto G = [&](int j) {
+    double acc = 0.0;
+    for (int t = 0; t < 11; ++t) {
+      const int q = j + t - 5;
+      if (q >= 0 && q < n) acc += A.win[t] * g[(int64_t)q * stride];
+    }
+    return acc;
+  };
+  double out = G(i);
+  if (i < 5) out += G(-i - 1);
+  if (i >= n - 5) out += G(2 * n - 1 - i);
+  return out;
+}
+
+__global__ void k_loss_adj_v(LossArgs A) {
+  const int64_t plane = (int64_t)A.h * A.w;
+  const int64_t tot = (int64_t)A.NI * A.S * plane;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
+  const int64_t bs = e / plane;
+  for (int k = 0; k < 3; ++k)
+    A.A3[k * tot + e] = adj_line(A, A.G3 + k * tot + bs * plane + c, A.w, A.h, r);
+}
+
+__global__ void k_loss_adj_h(LossArgs A) {
+  const int64_t plane = (int64_t)A.h * A.w;
+  const int64_t tot = (int64_t)A.NI * A.S * plane;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
+  const int64_t bs = e / plane;
+  const int s = (int)(bs % A.S), b = (int)(bs / A.S);
+  const double* rowp = A.A3 + bs * plane + (int64_t)r * A.w;
+  const double amx = adj_line(A, rowp, 1, A.w, c);
+  const double ab2 = adj_line(A, rowp + tot, 1, A.w, c);
+  const double aa2 = adj_line(A, rowp + 2 * tot, 1, A.w, c);
+  const double x = pred_at(A, b, s, r, c), y = gt_at(A, b, s, r, c);
+  const double n = (double)plane;
+  const double gssim = (amx + 2 * x * ab2 + y * aa2) / n;
+  const double diff = x - y;
+  const double sgn = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
+  const double gp = (1.0 - A.lam) * sgn / (n * A.S) - A.lam * gssim / A.S;
+  float* dz = A.dimg + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+  if (A.sup == 0) {
+    const float* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+    const double re = z[0], im = z[1];
+    const double m = hypot(re, im);
+    const double k = m > 0.0 ? gp / m : 0.0;
+    dz[0] = (float)(re * k);
+    dz[1] = (float)(im * k);
+  } else {
+    dz[s] = (float)gp;
+  }
+}
+
+__global__ void k_loss_finalize(LossArgs A) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= A.NI) return;
+  const double* sm = A.sums + (int64_t)b * (A.S + 2);
+  const double n = (double)A.h * A.w;
+  double ss = 0.0;
+  for (int s = 0; s < A.S; ++s) ss += sm[s] / n;
+  ss /= A.S;
+  const double l1 = sm[A.S] / (n * A.S);
+  A.stats[4 * b + 0] = (1.0 - A.lam) * l1 + A.lam * (1.0 - ss);
+  A.stats[4 * b + 1] = l1;
+  A.stats[4 * b + 2] = ss;
+  A.stats[4 * b + 3] = sm[A.S + 1] / (n * A.S);
+}
+
+int64_t loss_scratch_bytes(int NI, int h, int w, int C) {
+  const int64_t tot = (int64_t)NI * C * h * w;  // upper bound: S <= C
+  return (int64_t)sizeof(double) * (11 * tot + (int64_t)NI * (C + 2)) + 256;
+}
+
+int launch_loss(const float* img, const float* gt, int NI, int h, int w, int C, int sup,
+                double lam, float* dimg, double* stats, void* scratch, int64_t scratch_bytes,
+                cudaStream_t st) {
+  if (sup == 0 && C != 2) {
+    set_error("loss: magnitude supervision needs 2 channels, got %d", C);
+    return GSPARC_ERR_ARG;
+  }
+  if (h < 6 || w < 6) {
+    set_error("loss: image must be at least 6x6 for the 11-tap reflect window");
+    return GSPARC_ERR_ARG;
+  }
+  if (scratch_bytes < loss_scratch_bytes(NI, h, w, C)) {
+    set_error("loss: scratch too small");
+    return GSPARC_ERR_ARG;
+  }
+  LossArgs A;
+  make_window(A.win);
+  A.img = img;
+  A.gt = gt;
+  A.dimg = dimg;
+  A.NI = NI;
+  A.S = sup == 0 ? 1 : C;
+  A.C = C;
+  A.h = h;
+  A.w = w;
+  A.sup = sup;
+  A.lam = lam;
+  A.stats = stats;
+  const int64_t tot = (int64_t)NI * A.S * h * w;
+  double* base = (double*)scratch;
+  A.H5 = base;
+  A.G3 = A.H5 + 5 * tot;
+  A.A3 = A.G3 + 3 * tot;
+  A.sums = A.A3 + 3 * tot;
+  if (cudaMemsetAsync(A.sums, 0, sizeof(double) * NI * (A.S + 2), st) != cudaSuccess)
+    return check_launch("loss memset");
+  const unsigned blocks = (unsigned)((tot + 255) / 256);
+  k_loss_h<<<blocks, 256, 0, st>>>(A);
+  k_loss_v<<<blocks, 256, 0, st>>>(A);
+  k_loss_adj_v<<<blocks, 256, 0, st>>>(A);
+  k_loss_adj_h<<<blocks, 256, 0, st>>>(A);
+  k_loss_finalize<<<(NI + 127) / 128, 128, 0, st>>>(A);
+  return check_launch("k_loss");
+}
+
+}  // namespace gs

@@ -1,0 +1,200 @@
+// K1: per-Gaussian emitter MLP with 1/d attenuation, batched over TX.
+// Replaces mlp.direction_angles (mlp.py:83-89), mlp.batch_mlp_forward
+// (mlp.py:40-45), the near-plane distance clamp (rasterizer.py:103-105) and
+// coef = s / d_tx (rasterizer.py:200).  theta/phi are TX-independent and were
+// produced by K2 (rec32/rec64).  Output coef[i, b*C + c] (frame dtype).
+//
+// Two mappings:
+//   narrow: one thread per (Gaussian, TX); for small heads (C <= 8) where the
+//           130-float weight row is L1-resident across the TX threads.
+//   wide:   one warp per Gaussian; W2 (C x 16) streamed with coalesced float4
+//           loads (lane l reads float4 #l of the row block), partial dots
+//           reduced over the 4 lanes that share an output row.  This is the
+//           HBM-bound path of the 52-subcarrier config (7.5 KB per Gaussian).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gs {
+
+struct MlpArgs {
+  const float* w32;
+  const double* w64;
+  const double* pos;
+  const double* tx;  // [B,3]
+  const float4* rec32;
+  const double* rec64;
+  const uint64_t* key;
+  const int* live_list;  // nullptr -> all Gaussians (culled skipped)
+  const int* counters;
+  void* coef;
+  int64_t n;
+  int B, C, H, I, P;
+  int64_t Cp;  // B*C
+};
+
+__device__ __forceinline__ double tx_distance(const double* pos, const double* tx) {
+  double d0 = sub(pos[0], tx[0]), d1 = sub(pos[1], tx[1]), d2 = sub(pos[2], tx[2]);
+  double d = __dsqrt_rn(add(add(mul(d0, d0), mul(d1, d1)), mul(d2, d2)));
+  return d < NEAR_PLANE ? NEAR_PLANE : d;  // rasterizer.py:103-105
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gi = t / A.B;
+  const int b = (int)(t % A.B);
+  int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  if (gi >= count) return;
+  const int64_t i = A.live_list ? A.live_list[gi] : gi;
+  if (!A.live_list && A.key[i] == ~0ULL) return;
+  R theta, phi;
+  if constexpr (sizeof(R) == 4) {
+    float4 r = A.rec32[2 * i + 1];
+    theta = r.z;
+    phi = r.w;
+  } else {
+    theta = A.rec64[8 * i + 6];
+    phi = A.rec64[8 * i + 7];
+  }
+  const double* txb = A.tx + 3 * b;
+  R x[5] = {(R)txb[0], (R)txb[1], (R)txb[2], theta, phi};
+  const int H = A.H, I = A.I, C = A.C;
+  float hid32[32];
+  double hid64[32];
+  if constexpr (sizeof(R) == 4) {
+    const float* w = A.w32 + i * (int64_t)A.P;
+    for (int h = 0; h < H; ++h) {
+      float acc = 0.f;
+      for (int k = 0; k < I; ++k) acc += w[h * I + k] * x[k];
+      acc += w[H * I + h];
+      hid32[h] = acc > 0.f ? acc : 0.f;
+    }
+    const float* w2 = w + H * I + H;
+    const float* b2 = w2 + C * H;
+    double d = tx_distance(A.pos + 3 * i, txb);
+    float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+    for (int c = 0; c < C; ++c) {
+      float acc = 0.f;
+      for (int h = 0; h < H; ++h) acc += w2[c * H + h] * hid32[h];
+      acc += b2[c];
+      out[c] = (float)((double)acc / d);
+    }
+  } else {
+    const double* w = A.w64 + i * (int64_t)A.P;
+    for (int h = 0; h < H; ++h) {
+      double acc = 0.0;
+      for (int k = 0; k < I; ++k) acc += w[h * I + k] * x[k];
+      acc += w[H * I + h];
+      hid64[h] = acc > 0.0 ? acc : 0.0;
+    }
+    const double* w2 = w + H * I + H;
+    const double* b2 = w2 + C * H;
+    double d = tx_distance(A.pos + 3 * i, txb);
+    double* out = (double*)A.coef + i * A.Cp + (int64_t)b * C;
+    for (int c = 0; c < C; ++c) {
+      double acc = 0.0;
+      for (int h = 0; h < H; ++h) acc += w2[c * H + h] * hid64[h];
+      acc += b2[c];
+      out[c] = acc / d;
+    }
+  }
+}
+
+// Wide head, f32 weights, H == 16, I == 5, C % 4 == 0.
+__global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  if (gi >= count) return;
+  const int64_t i = A.live_list ? A.live_list[gi] : gi;
+  if (!A.live_list && A.key[i] == ~0ULL) return;
+  const float4 r1 = A.rec32[2 * i + 1];
+  const float* w = A.w32 + i * (int64_t)A.P;
+  const int C = A.C;
+  // W1 row for hidden unit `lane & 15`
+  const int hu = lane & 15;
+  float w1[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) w1[k] = __ldg(w + hu * 5 + k);
+  const float b1 = __ldg(w + 80 + hu);
+  const float4* w2v = reinterpret_cast<const float4*>(w + 96);
+  const float* b2 = w + 96 + 16 * C;
+  const int q = lane & 3;
+  const int nvec = 4 * C;
+  const double* p = A.pos + 3 * i;
+  for (int b = 0; b < A.B; ++b) {
+    const double* txb = A.tx + 3 * b;
+    float x[5] = {(float)txb[0], (float)txb[1], (float)txb[2], r1.z, r1.w};
+    float pre = 0.f;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) pre += w1[k] * x[k];
+    pre += b1;
+    float hid = pre > 0.f ? pre : 0.f;
+    float h0 = __shfl_sync(0xffffffffu, hid, 4 * q + 0);
+    float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
+    float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
+    float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
+    const double d = tx_distance(p, txb);
+    float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+    for (int f = lane; f < nvec; f += 32) {
+      float4 v = __ldg(w2v + f);
+      float part = v.x * h0 + v.y * h1 + v.z * h2 + v.w * h3;
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (q == 0) {
+        int o = f >> 2;
+        out[o] = (float)((double)(part + __ldg(b2 + o)) / d);
+      }
+    }
+  }
+}
+
+int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_only,
+               const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
+  MlpArgs A;
+  A.w32 = cloud.mlp_weights;
+  A.w64 = cloud.mlp_weights64;
+  A.pos = cloud.positions;
+  A.tx = tx;
+  A.rec32 = (const float4*)(frame + L.off_rec32);
+  A.rec64 = (const double*)(frame + L.off_rec64);
+  A.key = (const uint64_t*)(frame + L.off_key);
+  A.live_list = live_only ? (const int*)(frame + L.off_live_list) : nullptr;
+  A.counters = (const int*)(frame + L.off_counters);
+  A.coef = frame + L.off_coef;
+  A.n = cloud.n;
+  A.B = B;
+  A.C = cloud.mlp_out;
+  A.H = cloud.mlp_hidden;
+  A.I = cloud.mlp_in;
+  A.P = cloud.mlp_in * cloud.mlp_hidden + cloud.mlp_hidden + cloud.mlp_hidden * cloud.mlp_out +
+        cloud.mlp_out;
+  A.Cp = (int64_t)B * cloud.mlp_out;
+  if (A.Cp > L.channels) {
+    set_error("mlp: n_tx*mlp_out=%lld exceeds frame channels %lld", (long long)A.Cp,
+              (long long)L.channels);
+    return GSPARC_ERR_ARG;
+  }
+  if (A.H > 32 || A.I > 5) {
+    set_error("mlp: hidden<=32 and inputs==5 supported (got %d, %d)", A.H, A.I);
+    return GSPARC_ERR_UNSUPPORTED;
+  }
+  if (cloud.n == 0) return GSPARC_OK;
+  if (L.dtype == GSPARC_F64) {
+    if (!A.w64) {
+      set_error("mlp: f64 frame needs cloud.mlp_weights64");
+      return GSPARC_ERR_ARG;
+    }
+    int64_t threads = cloud.n * B;
+    k_mlp_narrow<double><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
+  } else if (A.C % 4 == 0 && A.C >= 16 && A.H == 16 && A.I == 5) {
+    int64_t threads = cloud.n * 32;
+    k_mlp_wide<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
+  } else {
+    int64_t threads = cloud.n * B;
+    k_mlp_narrow<float><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
+  }
+  return check_launch("k_mlp");
+}
+
+}  // namespace gs

@@ -1,0 +1,266 @@
+// K2: per-Gaussian preprocessing in f64 (one thread per Gaussian, source
+// order).  Replaces geometry.cull (geometry.py:198-224) and the geometry of
+// rasterizer._Prepared (rasterizer.py:75-102); the tile rectangle follows
+// rasterizer._tile_lists (rasterizer.py:117-141).  Arithmetic uses
+// round-to-nearest intrinsics in numpy's evaluation order so the depth key
+// (and therefore the sort order) is bit-identical to numpy's.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gs {
+
+struct PrepArgs {
+  gsparc_cloud cloud;
+  Pose pose;
+  GeoConst gc;
+  uint64_t* key;
+  float4* rec32;
+  double* rec64;
+  int4* rect;
+  int* counters;
+  int* tile_count;
+};
+
+__device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, double b0, double b1,
+                                           double b2) {
+  return add(add(mul(a0, b0), mul(a1, b1)), mul(a2, b2));
+}
+
+__device__ __forceinline__ double np_floor_div16(double v) { return floor(v / 16.0); }
+
+__global__ void __launch_bounds__(256) k_preprocess(PrepArgs A) {
+  extern __shared__ int s_tiles[];  // per-CTA tile histogram
+  const int ntiles = A.gc.ntx * A.gc.nty;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
+  __syncthreads();
+
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool kept_out = false;
+  int pairs_out = 0;
+  if (i < A.cloud.n) {
+    const double* P = A.cloud.positions + 3 * i;
+    const double* W = A.pose.W;
+    double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
+           p2 = sub(P[2], A.pose.rx[2]);
+    // (p - rx) @ W.T  (geometry.py:61-64)
+    double x = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
+    double y = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
+    double z = dot3_seq(p0, p1, p2, W[6], W[7], W[8]);
+    double xx = mul(x, x), yy = mul(y, y), zz = mul(z, z);
+    double r2 = add(add(xx, yy), zz);
+    double depth = __dsqrt_rn(r2);  // np.linalg.norm(axis=1)
+    bool keep = (depth >= NEAR_PLANE) && (depth <= FAR_PLANE);
+    // elevation >= -90 deg is a no-op except for NaN (geometry.py:210-212)
+    double sn = y / fmax(depth, 1e-30);
+    keep = keep && (sn == sn);
+
+    // projection (geometry.py:67-80), r == depth
+    double theta = atan2(x, z);
+    double mx = mul(add(theta / A.gc.pi, 1.0), A.gc.w * 0.5);
+    double c_sn = fmin(fmax(y / depth, -1.0), 1.0);
+    double el = asin(c_sn);
+    double my = mul(mul(2.0, el), A.gc.h / A.gc.pi);
+
+    // pole clamp (geometry.py:98-113, 131-138): points above 89 deg are
+    // evaluated at 89 deg with the same azimuth and radius
+    double jx = x, jy = y, jz = z;
+    const double rho2_u = add(xx, zz);
+    double jr2 = r2, rho2 = rho2_u;
+    if (el > A.gc.pole_lim) {
+      double tgt_rho = mul(depth, A.gc.cos_lim);
+      jx = mul(tgt_rho, sin(theta));
+      jy = mul(depth, A.gc.sin_lim);
+      jz = mul(tgt_rho, cos(theta));
+      double a = mul(jx, jx), b = mul(jy, jy), c = mul(jz, jz);
+      jr2 = add(add(a, b), c);
+      rho2 = add(a, c);
+    }
+    double rho = __dsqrt_rn(rho2);
+    const double ca = A.gc.ca, ce = A.gc.ce;
+    // J (geometry.py:143-148)
+    double J00 = mul(ca, jz) / rho2;
+    double J02 = mul(-ca, jx) / rho2;
+    double r2rho = mul(jr2, rho);
+    double J10 = mul(mul(-ce, jx), jy) / r2rho;
+    double J11 = mul(ce, rho) / jr2;
+    double J12 = mul(mul(-ce, jy), jz) / r2rho;
+
+    // Sigma = (R diag s)(R diag s)^T (scene.py:84-88, 117-139)
+    const double* q = A.cloud.rotations + 4 * i;
+    double qn = __dsqrt_rn(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
+                               mul(q[3], q[3])));
+    double qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
+    double R[3][3];
+    R[0][0] = 1.0 - 2.0 * add(mul(qy, qy), mul(qz, qz));
+    R[0][1] = 2.0 * sub(mul(qx, qy), mul(qw, qz));
+    R[0][2] = 2.0 * add(mul(qx, qz), mul(qw, qy));
+    R[1][0] = 2.0 * add(mul(qx, qy), mul(qw, qz));
+    R[1][1] = 1.0 - 2.0 * add(mul(qx, qx), mul(qz, qz));
+    R[1][2] = 2.0 * sub(mul(qy, qz), mul(qw, qx));
+    R[2][0] = 2.0 * sub(mul(qx, qz), mul(qw, qy));
+    R[2][1] = 2.0 * add(mul(qy, qz), mul(qw, qx));
+    R[2][2] = 1.0 - 2.0 * add(mul(qx, qx), mul(qy, qy));
+    const double* ls = A.cloud.log_scales + 3 * i;
+    double s0 = exp(ls[0]), s1 = exp(ls[1]), s2 = exp(ls[2]);
+    double M[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      M[r][0] = mul(R[r][0], s0);
+      M[r][1] = mul(R[r][1], s1);
+      M[r][2] = mul(R[r][2], s2);
+    }
+    double S[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        S[r][c] = add(add(mul(M[r][0], M[c][0]), mul(M[r][1], M[c][1])), mul(M[r][2], M[c][2]));
+    // V = W S W^T
+    double WS[3][3], V[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        WS[r][c] = add(add(mul(W[3 * r + 0], S[0][c]), mul(W[3 * r + 1], S[1][c])),
+                       mul(W[3 * r + 2], S[2][c]));
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        V[r][c] = add(add(mul(WS[r][0], W[3 * c + 0]), mul(WS[r][1], W[3 * c + 1])),
+                      mul(WS[r][2], W[3 * c + 2]));
+    // cov2d = J V J^T (rasterizer.py:92-95), J row 0 has J01 = 0
+    double JV0[3], JV1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      JV0[c] = add(mul(J00, V[0][c]), mul(J02, V[2][c]));
+      JV1[c] = add(add(mul(J10, V[0][c]), mul(J11, V[1][c])), mul(J12, V[2][c]));
+    }
+    double c00 = add(mul(JV0[0], J00), mul(JV0[2], J02));
+    double c01 = add(add(mul(JV0[0], J10), mul(JV0[1], J11)), mul(JV0[2], J12));
+    double c10 = add(mul(JV1[0], J00), mul(JV1[2], J02));
+    double c11 = add(add(mul(JV1[0], J10), mul(JV1[1], J11)), mul(JV1[2], J12));
+    double a = add(c00, COV2D_REG);
+    double b = mul(0.5, add(c01, c10));
+    double c = add(c11, COV2D_REG);
+    double det = sub(mul(a, c), mul(b, b));
+    double ry = mul(FOOTPRINT_SIGMA, __dsqrt_rn(fmax(c, 0.0)));
+    double rxr = mul(FOOTPRINT_SIGMA, __dsqrt_rn(a));
+    keep = keep && (add(my, ry) >= 0.0) && (sub(my, ry) <= (double)A.gc.h);
+
+    double logit = A.cloud.raw_opacities[i];
+    double opac;
+    if (logit >= 0.0) {
+      opac = 1.0 / (1.0 + exp(-logit));
+    } else {
+      double e = exp(logit);
+      opac = e / (1.0 + e);
+    }
+    double phi = atan2(y, __dsqrt_rn(rho2_u));  // mlp.py:88 (unclamped)
+
+    // tile rectangle (rasterizer.py:117-141)
+    const int ntx = A.gc.ntx, nty = A.gc.nty;
+    const double wd = (double)A.gc.w;
+    int y0 = 0, y1 = -1, a0 = 0, a1 = -1, b0 = 0, b1 = -1, npairs = 0;
+    if (keep) {
+      double fy0 = floor(sub(sub(my, ry), 0.5) / 16.0);
+      double fy1 = floor(add(add(my, ry), 0.5) / 16.0);
+      y0 = (int)fmin(fmax(fy0, 0.0), (double)(nty - 1));
+      y1 = (int)fmin(fmax(fy1, 0.0), (double)(nty - 1));
+      double lo = sub(sub(mx, rxr), 0.5);
+      {  // np.mod
+        double m = fmod(lo, wd);
+        if (m != 0.0) {
+          if ((wd < 0.0) != (m < 0.0)) m = add(m, wd);
+        } else {
+          m = 0.0;
+        }
+        lo = m;
+      }
+      double span = add(mul(2.0, rxr), 1.0);
+      if (span >= wd) {
+        a0 = 0;
+        a1 = ntx - 1;
+      } else {
+        double hi = add(lo, span);
+        a0 = (int)np_floor_div16(lo);
+        if (hi < wd) {
+          a1 = (int)np_floor_div16(hi);
+        } else {
+          a1 = ntx - 1;
+          b0 = 0;
+          b1 = (int)np_floor_div16(sub(hi, wd));
+        }
+      }
+      npairs = (y1 - y0 + 1) * ((a1 - a0 + 1) + (b1 - b0 + 1));
+    }
+
+    uint64_t k = keep ? (uint64_t)__double_as_longlong(depth) : ~0ULL;
+    A.key[i] = k;
+    A.rec32[2 * i] = make_float4((float)mx, (float)my, (float)(c / det), (float)(-b / det));
+    A.rec32[2 * i + 1] = make_float4((float)(a / det), (float)opac, (float)theta, (float)phi);
+    if (A.rec64) {
+      double* r = A.rec64 + 8 * i;
+      r[0] = mx;
+      r[1] = my;
+      r[2] = c / det;
+      r[3] = -b / det;
+      r[4] = a / det;
+      r[5] = opac;
+      r[6] = theta;
+      r[7] = phi;
+    }
+    A.rect[i] = make_int4(y0 | (y1 << 16), (a0 & 0xffff) | (a1 << 16), (b0 & 0xffff) | (b1 << 16),
+                          npairs);
+    if (keep) {
+      for (int ty = y0; ty <= y1; ++ty) {
+        for (int tx = a0; tx <= a1; ++tx) atomicAdd(s_tiles + ty * ntx + tx, 1);
+        for (int tx = b0; tx <= b1; ++tx) atomicAdd(s_tiles + ty * ntx + tx, 1);
+      }
+    }
+    kept_out = keep;
+    pairs_out = npairs;
+  }
+  {
+    unsigned kept_warp = __reduce_add_sync(0xffffffffu, kept_out ? 1u : 0u);
+    unsigned pairs_warp = __reduce_add_sync(0xffffffffu, (unsigned)pairs_out);
+    if ((threadIdx.x & 31) == 0) {
+      if (kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
+      if (pairs_warp) atomicAdd(A.counters + GSPARC_CNT_PAIRS, (int)pairs_warp);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    int v = s_tiles[t];
+    if (v) atomicAdd(A.tile_count + t, v);
+  }
+}
+
+int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
+                      const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
+  PrepArgs A;
+  A.cloud = cloud;
+  for (int k = 0; k < 3; ++k) A.pose.rx[k] = view.rx[k];
+  for (int k = 0; k < 9; ++k) A.pose.W[k] = view.rotation[k];
+  A.gc = make_geo_const(L.width, L.height);
+  A.key = (uint64_t*)(frame + L.off_key);
+  A.rec32 = (float4*)(frame + L.off_rec32);
+  A.rec64 = L.dtype == GSPARC_F64 ? (double*)(frame + L.off_rec64) : nullptr;
+  A.rect = (int4*)(frame + L.off_rect);
+  A.counters = (int*)(frame + L.off_counters);
+  A.tile_count = (int*)(frame + L.off_tile_count);
+  if (cudaMemsetAsync(frame + L.off_counters, 0, GSPARC_NUM_COUNTERS * sizeof(int), st) !=
+          cudaSuccess ||
+      cudaMemsetAsync(frame + L.off_tile_count, 0, sizeof(int) * L.ntiles, st) != cudaSuccess)
+    return check_launch("preprocess memset");
+  if (cloud.n > 0) {
+    int blocks = (int)((cloud.n + 255) / 256);
+    size_t smem = sizeof(int) * (size_t)L.ntiles;
+    k_preprocess<<<blocks, 256, smem, st>>>(A);
+  }
+  return check_launch("k_preprocess");
+}
+
+}  // namespace gs

@@ -1,0 +1,217 @@
+// K5: per-tile backward of the compositing, back to front.
+// Replaces the per-tile loop of rasterizer.rasterize_backward
+// (rasterizer.py:286-326).  Instead of the reference's f64 front-to-back
+// cumprod + reverse cumsum, each pixel walks its included range backwards
+// from the stored final transmittance (T_before = T_after / (1 - alpha),
+// SPEC.md rasterize_backward "re-deriving each T_i from stored final
+// transmittance"), keeping the suffix sum  S_k = sum_{j>k} wgt_j (u . c_j)
+// exactly as accumulated, which avoids the cancellation of total - prefix.
+//
+// Gradients are linear in dL, so channels are split into chunks of CB
+// (grid.y); every chunk contributes its share of dL/dalpha to the geometric
+// accumulators.  Per batch:
+//   * scan: per pixel, d alpha, d(sigma g), d conic, d mean2d (reduced over
+//     the warp by shuffles, over the CTA in shared memory);
+//   * dL/dcoef[k, c] = sum_p wgt[k,p] u[p,c] as a shared-memory GEMM over the
+//     tile's 256 pixels;
+//   * one global atomicAdd per (Gaussian, tile, value).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gs {
+
+struct BwdArgs {
+  const uint64_t* pairs;
+  const int* tile_start;
+  const int* tile_stop;
+  const float4* rec32;
+  const double* rec64;
+  const void* coef;
+  const void* dL;  // [B,h,w,C]
+  const void* T_final;
+  const int* last;
+  void* gcoef;  // [n, Cp]
+  void* ggeo;   // [n, 8]
+  const int* counters;
+  int64_t Cp;
+  int C;
+  int w, h, ntx;
+};
+
+template <typename R, int CB, int NB>
+__global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  R* s_u = (R*)smraw;                    // [CB][256]
+  R* s_wgt = s_u + CB * TILE_PX;         // [NB][256]
+  R* s_coef = s_wgt + NB * TILE_PX;      // [NB][CB]
+  R* s_red = s_coef + NB * CB;           // [NB][6]
+  Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6);  // [NB]
+  int* s_idx = (int*)(s_rec + NB);       // [NB]
+
+  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const int tile = blockIdx.x, chunk = blockIdx.y;
+  const int tid = threadIdx.x, pix = tid;
+  const int lane = tid & 31;
+  const int tx_ = tile % A.ntx, ty = tile / A.ntx;
+  const int px = tx_ * TILE + (pix & (TILE - 1)), py = ty * TILE + pix / TILE;
+  const bool inside = px < A.w && py < A.h;
+  const int start = A.tile_start[tile];
+  const int nvisit = A.tile_stop[tile];
+  if (nvisit == 0) return;
+  const int chunk_base = chunk * CB;
+  const R pcx = (R)px + R(0.5), pcy = (R)py + R(0.5);
+  const R wR = (R)A.w, half_w = (R)(A.w / 2.0);
+  const R amax = sizeof(R) == 4 ? R(ALPHA_MAX_F) : R(ALPHA_MAX);
+
+  R u[CB];
+  const R* dL = (const R*)A.dL;
+#pragma unroll
+  for (int c = 0; c < CB; ++c) {
+    const int64_t cc = chunk_base + c;
+    R v = R(0);
+    if (inside && cc < A.Cp) {
+      const int64_t b = cc / A.C, ch = cc - b * A.C;
+      v = dL[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch];
+    }
+    u[c] = v;
+    s_u[c * TILE_PX + pix] = v;
+  }
+  const int p = py * A.w + px;
+  R T = inside ? ((const R*)A.T_final)[p] : R(1);
+  const int lastp = inside ? A.last[p] : 0;
+  R suffix = R(0);
+
+  R* gcoef = (R*)A.gcoef;
+  R* ggeo = (R*)A.ggeo;
+  const R* coef = (const R*)A.coef;
+
+  for (int bend = nvisit; bend > 0; bend -= NB) {
+    const int b0 = bend > NB ? bend - NB : 0;
+    const int nb = bend - b0;
+    __syncthreads();
+    if (tid < nb) {
+      const uint32_t idx = (uint32_t)A.pairs[start + b0 + tid];
+      s_idx[tid] = (int)idx;
+      s_rec[tid] = load_rec_t<R>(A.rec32, A.rec64, idx);
+    }
+    for (int e = tid; e < nb * CB; e += blockDim.x) {
+      const int j = e / CB, c = e - j * CB;
+      const uint32_t idx = (uint32_t)A.pairs[start + b0 + j];
+      const int64_t cc = chunk_base + c;
+      s_coef[e] = cc < A.Cp ? coef[(int64_t)idx * A.Cp + cc] : R(0);
+    }
+    for (int e = tid; e < nb * 6; e += blockDim.x) s_red[e] = R(0);
+    __syncthreads();
+    for (int j = nb - 1; j >= 0; --j) {
+      const int k = b0 + j;
+      R wgt = R(0), g_sig = R(0), gc0 = R(0), gc1 = R(0), gc2 = R(0), gm0 = R(0), gm1 = R(0);
+      if (k < lastp) {
+        const Rec<R> r = s_rec[j];
+        const AlphaOut<R> a =
+            pixel_alpha<R>(pcx, pcy, r.mx, r.my, r.ca, r.cb, r.cc, r.op, wR, half_w);
+        if (a.alpha > R(0)) {
+          const R om = R(1) - a.alpha;
+          const R Tb = T / om;
+          wgt = Tb * a.alpha;
+          R uc = R(0);
+          const R* cf = s_coef + j * CB;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) uc += u[c] * cf[c];
+          const R dA = Tb * uc - suffix / om;
+          suffix += wgt * uc;
+          T = Tb;
+          if (a.raw < amax) {
+            g_sig = dA * a.g;
+            const R dq = R(-0.5) * (dA * r.op) * a.g;
+            gc0 = dq * a.dx * a.dx;
+            gc1 = dq * a.dx * a.dy;
+            gc2 = dq * a.dy * a.dy;
+            gm0 = -(dq * R(2) * (r.ca * a.dx + r.cb * a.dy));
+            gm1 = -(dq * R(2) * (r.cb * a.dx + r.cc * a.dy));
+          }
+        }
+      }
+      s_wgt[j * TILE_PX + pix] = wgt;
+      const bool any = __any_sync(0xffffffffu, g_sig != R(0) || gc0 != R(0) || gc2 != R(0) ||
+                                                   gm0 != R(0) || gm1 != R(0));
+      if (any) {
+        g_sig = warp_sum(g_sig);
+        gc0 = warp_sum(gc0);
+        gc1 = warp_sum(gc1);
+        gc2 = warp_sum(gc2);
+        gm0 = warp_sum(gm0);
+        gm1 = warp_sum(gm1);
+        if (lane == 0) {
+          R* rr = s_red + j * 6;
+          atomicAdd(rr + 0, gc0);
+          atomicAdd(rr + 1, gc1);
+          atomicAdd(rr + 2, gc2);
+          atomicAdd(rr + 3, gm0);
+          atomicAdd(rr + 4, gm1);
+          atomicAdd(rr + 5, g_sig);
+        }
+      }
+    }
+    __syncthreads();
+    // dL/dcoef for this batch: [nb x CB] = wgt[nb x 256] . u[256 x CB]
+    for (int o = tid; o < nb * CB; o += blockDim.x) {
+      const int j = o / CB, c = o - j * CB;
+      const int64_t cc = chunk_base + c;
+      if (cc >= A.Cp) continue;
+      const R* wr = s_wgt + j * TILE_PX;
+      const R* ur = s_u + c * TILE_PX;
+      R s = R(0);
+#pragma unroll 8
+      for (int q = 0; q < TILE_PX; ++q) s += wr[q] * ur[q];
+      if (s != R(0)) atomicAdd(gcoef + (int64_t)s_idx[j] * A.Cp + cc, s);
+    }
+    for (int o = tid; o < nb * 6; o += blockDim.x) {
+      const R v = s_red[o];
+      if (v != R(0)) atomicAdd(ggeo + (int64_t)s_idx[o / 6] * 8 + (o % 6), v);
+    }
+  }
+}
+
+template <typename R, int CB, int NB>
+static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
+  const size_t smem = sizeof(R) * ((size_t)CB * TILE_PX + (size_t)NB * TILE_PX + NB * CB + NB * 6) +
+                      sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
+  auto kern = k_raster_bwd<R, CB, NB>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int chunks = (int)((A.Cp + CB - 1) / CB);
+  kern<<<dim3(ntiles, chunks), 256, smem, st>>>(A);
+  return check_launch("k_raster_bwd");
+}
+
+int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
+                           const void* dL, cudaStream_t st) {
+  BwdArgs A;
+  A.pairs = (const uint64_t*)(frame + L.off_pairs);
+  A.tile_start = (const int*)(frame + L.off_tile_start);
+  A.tile_stop = (const int*)(frame + L.off_tile_stop);
+  A.rec32 = (const float4*)(frame + L.off_rec32);
+  A.rec64 = (const double*)(frame + L.off_rec64);
+  A.coef = frame + L.off_coef;
+  A.dL = dL;
+  A.T_final = frame + L.off_T;
+  A.last = (const int*)(frame + L.off_last);
+  A.gcoef = frame + L.off_gcoef;
+  A.ggeo = frame + L.off_ggeo;
+  A.counters = (const int*)(frame + L.off_counters);
+  A.Cp = (int64_t)n_tx * C;
+  A.C = C;
+  A.w = L.width;
+  A.h = L.height;
+  A.ntx = L.ntx;
+  const size_t esz = L.dtype == GSPARC_F64 ? 8 : 4;
+  if (cudaMemsetAsync(A.gcoef, 0, esz * (size_t)L.n * (size_t)L.channels, st) != cudaSuccess ||
+      cudaMemsetAsync(A.ggeo, 0, esz * (size_t)L.n * 8, st) != cudaSuccess)
+    return check_launch("bwd memset");
+  if (L.dtype == GSPARC_F64) return launch_bwd_cfg<double, 4, 32>(A, L.ntiles, st);
+  if (A.Cp <= 2) return launch_bwd_cfg<float, 2, 32>(A, L.ntiles, st);
+  if (A.Cp <= 8) return launch_bwd_cfg<float, 8, 32>(A, L.ntiles, st);
+  if (A.Cp <= 16) return launch_bwd_cfg<float, 16, 32>(A, L.ntiles, st);
+  return launch_bwd_cfg<float, 32, 32>(A, L.ntiles, st);
+}
+
+}  // namespace gs

@@ -1,0 +1,193 @@
+"""GPU parity of the forward path (K2 preprocess, K3 binning/sort, K1 MLP,
+K4 raster) against the golden vectors of the real reference and the CPU
+oracle.  Mirrors /root/reference/pkg/tests/test_rasterizer.py:32-154.
+
+Bars (north_star): tile lists and depth order bit-exact; images within 1e-4
+normwise (max|gpu-ref| / max|ref|) in fp32; contributor-count threshold flips
+reported and bounded."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, golden_cloud
+
+pytestmark = pytest.mark.gpu
+
+RX, W = np.zeros(3), np.eye(3)
+F32_TOL = 1e-4     # normwise, fp32 path (north_star)
+F64_TOL = 1e-12    # normwise, f64 verification path
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2511_22793_b200 import rasterizer
+    return rasterizer
+
+
+@pytest.fixture(scope="module")
+def pose():
+    from paper_2511_22793_b200 import ViewPose
+    return ViewPose(np.zeros(3))
+
+
+def host_cloud(oc):
+    from paper_2511_22793_b200 import GaussianCloud
+    return GaussianCloud(oc.positions, oc.log_scales, oc.rotations,
+                         oc.raw_opacities, oc.mlp_weights, oc.mlp_dims)
+
+
+def normwise(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+def assert_tiles_equal(aux, fx):
+    got = aux.tile_sources()
+    keys = [tuple(k) for k in fx["tile_keys"]]
+    assert sorted(got) == keys
+    ofs = fx["tile_offsets"]
+    for t, k in enumerate(keys):
+        ref = fx["tile_src"][ofs[t]:ofs[t + 1]]
+        assert np.array_equal(got[k], ref), f"tile {k}"
+
+
+GOLD = ["ka_single", "ka_two", "ka_clamp", "ka_near", "rand96_0", "rand96_1",
+        "rand96_2", "f64_noexit", "seam", "seam_dup", "bwd4", "bwd64",
+        "bench512"]
+
+
+@pytest.mark.parametrize("case", GOLD)
+def test_forward_matches_golden(case, R, pose):
+    fx = golden(case)
+    cloud = host_cloud(golden_cloud(fx))
+    dt = np.dtype(str(fx["dtype"])).type
+    img, aux = R.rasterize_forward(cloud, pose, fx["tx"], int(fx["w"]),
+                                   int(fx["h"]), dtype=dt,
+                                   t_eps=float(fx["t_eps"]))
+    assert img.data.dtype == fx["img"].dtype
+    assert_tiles_equal(aux, fx)
+    tol = F32_TOL if dt == np.float32 else F64_TOL
+    assert normwise(img.data, fx["img"]) <= tol
+    flips = int((aux.contrib_count != fx["count"]).sum())
+    assert flips <= max(2, fx["count"].size // 10000), flips
+    assert np.abs(aux.transmittance - fx["T"]).max() <= \
+        (1e-5 if dt == np.float32 else 1e-12)
+    if "ref" in fx:
+        assert normwise(img.data, fx["ref"]) <= tol
+
+
+def test_known_values(R, pose):
+    from paper_2511_22793_b200 import GaussianCloud, pixel_to_direction
+    P = 130
+    w_ = np.zeros((1, P))
+    w_[0, -2:] = (0.8, -0.6)
+    d = 2.0 * pixel_to_direction(18, 4, 36, 9)
+    c = GaussianCloud(d.reshape(1, 3), np.full((1, 3), np.log(0.15)),
+                      np.array([[1.0, 0, 0, 0]]), np.zeros((1, 1)), w_)
+    img, aux = R.rasterize_forward(c, pose, [0.0, 0.0, 0.0], 36, 9)
+    assert np.allclose(img.data[4, 18], [0.2, -0.15], atol=1e-6)
+    assert np.isclose(aux.transmittance[4, 18], 0.5, atol=1e-6)
+    assert aux.contrib_count[4, 18] == 1
+    assert abs(img.data[4, 25, 0]) < abs(img.data[4, 18, 0])
+
+
+def test_prepare_depth_order_and_records(R, pose):
+    fx = golden("bench512")
+    cloud = host_cloud(golden_cloud(fx))
+    _, aux = R.rasterize_forward(cloud, pose, fx["tx"], 360, 90)
+    pr = aux.prep
+    assert np.array_equal(pr.idx, fx["prep_idx"])
+    assert np.array_equal(pr.depth, fx["prep_depth"])      # bit-exact keys
+    assert np.abs(pr.mean2d - fx["prep_mean2d"]).max() <= 1e-4  # f32 record
+    assert normwise(pr.conic, fx["prep_conic"]) <= 1e-6
+    _, aux64 = R.rasterize_forward(cloud, pose, fx["tx"], 360, 90,
+                                   dtype=np.float64)
+    p64 = aux64.prep
+    assert np.abs(p64.mean2d - fx["prep_mean2d"]).max() <= 1e-10
+    assert normwise(p64.conic, fx["prep_conic"]) <= 1e-12
+    assert np.abs(p64.opac - fx["prep_opac"]).max() <= 1e-15
+
+
+def test_multichannel_f2(R, pose):
+    fx = golden("csi_f2")
+    cloud = host_cloud(golden_cloud(fx))
+    img, _ = R.rasterize_forward(cloud, pose, fx["tx"], 180, 45,
+                                 dtype=np.float64, t_eps=0.0)
+    assert img.data.shape == (45, 180, 4)
+    assert normwise(img.data, fx["img"]) <= F64_TOL
+    img32, _ = R.rasterize_forward(cloud, pose, fx["tx"], 180, 45)
+    assert normwise(img32.data, fx["ref"]) <= F32_TOL
+
+
+@pytest.mark.parametrize("n,F,kind", [(4096, 1, "bench"), (2048, 1, "pert"),
+                                      (1500, 4, "bench"), (3000, 52, "bench")])
+def test_against_oracle_at_scale(n, F, kind, R, pose):
+    oc = O.bench_scene(n, F=F) if kind == "bench" else \
+        O.round_f32(O.perturbed_scene(n, seed=1, F=F))
+    tx = O.sample_tx(5, 1)[0]
+    ref, aux_ref = O.forward(oc, RX, W, tx, 360, 90, threads=8)
+    img, aux = R.rasterize_forward(host_cloud(oc), pose, tx, 360, 90)
+    # bit-exact tile lists (source indices in compositing order)
+    got = aux.tile_sources()
+    want = {k: aux_ref.prep.idx[v] for k, v in aux_ref.tiles.items()}
+    assert sorted(got) == sorted(want)
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k
+    assert normwise(img.data, ref) <= F32_TOL
+    flips = int((aux.contrib_count != aux_ref.contrib_count).sum())
+    assert flips <= 4, flips
+
+
+def test_batched_tx_equals_single(R, pose):
+    from paper_2511_22793_b200 import DeviceCloud
+    oc = O.bench_scene(2000)
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    txs = O.sample_tx(9, 8)
+    batch, _ = R.rasterize_forward_batch(dc, pose, txs, 360, 90)
+    batch = batch.cpu().numpy()
+    for b in range(8):
+        one, _ = R.rasterize_forward(dc, pose, txs[b], 360, 90)
+        assert normwise(batch[b], one.data) <= 1e-6
+
+
+def test_lazy_mlp_equals_fused(R, pose):
+    from paper_2511_22793_b200 import DeviceCloud
+    oc = O.bench_scene(3000, F=8)
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    tx = O.sample_tx(2, 1)
+    a, fa = R.rasterize_forward_batch(dc, pose, tx, 360, 90, lazy=False)
+    b, fb = R.rasterize_forward_batch(dc, pose, tx, 360, 90, lazy=True)
+    assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+    assert np.array_equal(fa.contrib_count().cpu().numpy(),
+                          fb.contrib_count().cpu().numpy())
+
+
+def test_deterministic_and_dtype(R, pose):
+    oc = O.perturbed_scene(64, seed=13)
+    a, _ = R.rasterize_forward(host_cloud(oc), pose, [0, 1, 0.5], 180, 45)
+    b, _ = R.rasterize_forward(host_cloud(oc), pose, [0, 1, 0.5], 180, 45)
+    assert a.data.dtype == np.float32
+    assert np.array_equal(a.data, b.data)
+
+
+def test_permutation_invariance(R, pose):
+    oc = O.perturbed_scene(40, seed=12)
+    perm = np.random.default_rng(0).permutation(40)
+    sh = O.Cloud(*(getattr(oc, g)[perm] for g in O.GROUPS))
+    a = R.rasterize_reference(host_cloud(oc), pose, [0, 0, 0], 90, 30)
+    b = R.rasterize_reference(host_cloud(sh), pose, [0, 0, 0], 90, 30)
+    assert np.abs(a.data - b.data).max() <= 1e-12
+
+
+def test_culled_scene(R, pose):
+    from paper_2511_22793_b200 import GaussianCloud
+    c = GaussianCloud(np.array([[0.0, -50.0, 1.0]]), np.full((1, 3), -1.0),
+                      np.array([[1.0, 0, 0, 0]]), np.zeros((1, 1)),
+                      np.ones((1, 130)))
+    img, aux = R.rasterize_forward(c, pose, [0, 0, 0], 36, 9)
+    assert not img.data.any()
+    assert np.all(aux.transmittance == 1.0)
+    g = R.rasterize_backward(np.ones((9, 36, 2)), c, pose, [0, 0, 0], aux)
+    assert not g.positions.any() and not g.mlp_weights.any()
