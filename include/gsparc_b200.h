@@ -177,12 +177,13 @@ int64_t gsparc_loss_scratch_bytes(int32_t n_img, int32_t height, int32_t width,
 /* K7: per image b: pred = |img| (supervision 0, C must be 2) or img
  * (supervision 1); loss = (1-lam) L1 + lam (1 - SSIM) (11x11 Gaussian window,
  * sigma 1.5, reflect padding); dimg = dloss/dimg chained through the
- * magnitude.  img/gt/dimg f32; gt has 1 (magnitude) or C channels.
+ * magnitude.  img/gt/dimg in `dtype` (GSPARC_F32 / GSPARC_F64); gt has
+ * 1 (magnitude) or C channels; arithmetic is f64.
  * stats_out: f64 [n_img, 4] = (loss, l1, ssim, mse) per image. */
-int gsparc_loss_fwd_bwd(const float* img_dev, const float* gt_dev,
-                        int32_t n_img, int32_t height, int32_t width,
-                        int32_t channels, int32_t supervision, double lam,
-                        float* dimg_dev, double* stats_out_dev,
+int gsparc_loss_fwd_bwd(const void* img_dev, const void* gt_dev,
+                        int32_t dtype, int32_t n_img, int32_t height,
+                        int32_t width, int32_t channels, int32_t supervision,
+                        double lam, void* dimg_dev, double* stats_out_dev,
                         void* scratch_dev, int64_t scratch_bytes,
                         void* stream);
 

@@ -91,8 +91,8 @@ def lib():
                                            c_i32, c_vp]),
         "gsparc_loss_scratch_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
         "gsparc_loss_fwd_bwd": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32,
-                                        c_i32, c_dbl, c_vp, c_vp, c_vp, c_i64,
-                                        c_vp]),
+                                        c_i32, c_i32, c_dbl, c_vp, c_vp, c_vp,
+                                        c_i64, c_vp]),
         "gsparc_adam_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                      c_vp, c_vp, c_vp, c_vp, c_vp,
                                      P(CAdamConfig), c_vp]),

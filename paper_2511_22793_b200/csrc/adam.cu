@@ -59,7 +59,8 @@ __device__ double position_lr_dev(double step, const gsparc_adam_config& c) {
 }
 
 __global__ void k_adam(AdamArgs A, int64_t total) {
-  if (A.counters[GSPARC_CNT_NONFINITE]) return;
+  // a frame whose pair buffer overflowed produced no valid gradient
+  if (A.counters[GSPARC_CNT_NONFINITE] || A.counters[GSPARC_CNT_OVERFLOW]) return;
   const int64_t step = *A.step;
   const double t = (double)(step + 1);
   const double b1 = A.cfg.beta1, b2 = A.cfg.beta2, eps = A.cfg.eps;
@@ -88,7 +89,7 @@ __global__ void k_adam(AdamArgs A, int64_t total) {
 }
 
 __global__ void k_adam_finish(AdamArgs A) {
-  const bool skip = A.counters[GSPARC_CNT_NONFINITE] != 0;
+  const bool skip = A.counters[GSPARC_CNT_NONFINITE] != 0 || A.counters[GSPARC_CNT_OVERFLOW] != 0;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (!skip && i < A.n) {  // normalize_quaternions (scene.py:117-122)
     double* q = A.rot + 4 * i;

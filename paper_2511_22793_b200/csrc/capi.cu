@@ -239,17 +239,18 @@ int64_t gsparc_loss_scratch_bytes(int32_t n_img, int32_t height, int32_t width,
   return loss_scratch_bytes(n_img, height, width, channels);
 }
 
-int gsparc_loss_fwd_bwd(const float* img_dev, const float* gt_dev, int32_t n_img,
+int gsparc_loss_fwd_bwd(const void* img_dev, const void* gt_dev, int32_t dtype, int32_t n_img,
                         int32_t height, int32_t width, int32_t channels, int32_t supervision,
-                        double lam, float* dimg_dev, double* stats_out_dev, void* scratch_dev,
+                        double lam, void* dimg_dev, double* stats_out_dev, void* scratch_dev,
                         int64_t scratch_bytes, void* stream) {
   if (!img_dev || !gt_dev || !dimg_dev || !stats_out_dev || !scratch_dev || n_img < 1 ||
-      channels < 1 || (supervision != 0 && supervision != 1)) {
+      channels < 1 || (supervision != 0 && supervision != 1) ||
+      (dtype != GSPARC_F32 && dtype != GSPARC_F64)) {
     set_error("loss_fwd_bwd: invalid arguments");
     return GSPARC_ERR_ARG;
   }
-  return launch_loss(img_dev, gt_dev, n_img, height, width, channels, supervision, lam, dimg_dev,
-                     stats_out_dev, scratch_dev, scratch_bytes, (cudaStream_t)stream);
+  return launch_loss(img_dev, gt_dev, dtype, n_img, height, width, channels, supervision, lam,
+                     dimg_dev, stats_out_dev, scratch_dev, scratch_bytes, (cudaStream_t)stream);
 }
 
 int gsparc_adam_step(double* positions, double* log_scales, double* rotations,

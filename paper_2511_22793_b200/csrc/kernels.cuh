@@ -19,8 +19,8 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
                           int B, const gsparc_frame_layout& L, char* frame, void* grad,
                           int grad_dtype, cudaStream_t st);
 int64_t loss_scratch_bytes(int NI, int h, int w, int C);
-int launch_loss(const float* img, const float* gt, int NI, int h, int w, int C, int sup,
-                double lam, float* dimg, double* stats, void* scratch, int64_t scratch_bytes,
+int launch_loss(const void* img, const void* gt, int dtype, int NI, int h, int w, int C, int sup,
+                double lam, void* dimg, double* stats, void* scratch, int64_t scratch_bytes,
                 cudaStream_t st);
 int launch_adam(double* pos, double* ls, double* rot, double* op, float* mlp, int64_t n, int P,
                 const float* g, float* m, float* v, int64_t* step, int* counters,

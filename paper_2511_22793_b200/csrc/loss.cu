@@ -24,11 +24,12 @@ static void make_window(double* w) {
   for (int t = 0; t < 11; ++t) w[t] /= s;
 }
 
-struct LossArgs {
+template <typename T>
+struct LossArgsT {
   double win[11];
-  const float* img;
-  const float* gt;
-  float* dimg;
+  const T* img;
+  const T* gt;
+  T* dimg;
   double* H5;    // [5][NI][S][h][w]
   double* G3;    // [3][NI][S][h][w]
   double* A3;    // [3][NI][S][h][w]
@@ -44,16 +45,19 @@ __device__ __forceinline__ int refl(int j, int n) {
   return j;
 }
 
-__device__ __forceinline__ double pred_at(const LossArgs& A, int b, int s, int r, int c) {
-  const float* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+template <typename T>
+__device__ __forceinline__ double pred_at(const LossArgsT<T>& A, int b, int s, int r, int c) {
+  const T* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
   if (A.sup == 0) return hypot((double)z[0], (double)z[1]);
   return (double)z[s];
 }
-__device__ __forceinline__ double gt_at(const LossArgs& A, int b, int s, int r, int c) {
+template <typename T>
+__device__ __forceinline__ double gt_at(const LossArgsT<T>& A, int b, int s, int r, int c) {
   return (double)A.gt[(((int64_t)b * A.h + r) * A.w + c) * A.S + s];
 }
 
-__global__ void k_loss_h(LossArgs A) {
+template <typename T>
+__global__ void k_loss_h(LossArgsT<T> A) {
   const int64_t plane = (int64_t)A.h * A.w;
   const int64_t tot = (int64_t)A.NI * A.S * plane;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -75,7 +79,8 @@ __global__ void k_loss_h(LossArgs A) {
   for (int k = 0; k < 5; ++k) A.H5[k * tot + e] = a[k];
 }
 
-__global__ void k_loss_v(LossArgs A) {
+template <typename T>
+__global__ void k_loss_v(LossArgsT<T> A) {
   const int64_t plane = (int64_t)A.h * A.w;
   const int64_t tot = (int64_t)A.NI * A.S * plane;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,7 +139,8 @@ __global__ void k_loss_v(LossArgs A) {
 
 // adjoint along rows: out[r] = G(r) + [r<5] G(-r-1) + [r>=h-5] G(2h-1-r),
 // G(j) = sum_t w[t] g[j+t-5] (g = 0 outside [0,h))
-__device__ __forceinline__ double adj_line(const LossArgs& A, const double* g, int stride, int n,
+template <typename T>
+__device__ __forceinline__ double adj_line(const LossArgsT<T>& A, const double* g, int stride, int n,
                                           int i) {
   auto G = [&](int j) {
     double acc = 0.0;
@@ -150,7 +156,8 @@ __device__ __forceinline__ double adj_line(const LossArgs& A, const double* g, i
   return out;
 }
 
-__global__ void k_loss_adj_v(LossArgs A) {
+template <typename T>
+__global__ void k_loss_adj_v(LossArgsT<T> A) {
   const int64_t plane = (int64_t)A.h * A.w;
   const int64_t tot = (int64_t)A.NI * A.S * plane;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -161,7 +168,8 @@ __global__ void k_loss_adj_v(LossArgs A) {
     A.A3[k * tot + e] = adj_line(A, A.G3 + k * tot + bs * plane + c, A.w, A.h, r);
 }
 
-__global__ void k_loss_adj_h(LossArgs A) {
+template <typename T>
+__global__ void k_loss_adj_h(LossArgsT<T> A) {
   const int64_t plane = (int64_t)A.h * A.w;
   const int64_t tot = (int64_t)A.NI * A.S * plane;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -179,20 +187,21 @@ __global__ void k_loss_adj_h(LossArgs A) {
   const double diff = x - y;
   const double sgn = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
   const double gp = (1.0 - A.lam) * sgn / (n * A.S) - A.lam * gssim / A.S;
-  float* dz = A.dimg + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+  T* dz = A.dimg + (((int64_t)b * A.h + r) * A.w + c) * A.C;
   if (A.sup == 0) {
-    const float* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
+    const T* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
     const double re = z[0], im = z[1];
     const double m = hypot(re, im);
     const double k = m > 0.0 ? gp / m : 0.0;
-    dz[0] = (float)(re * k);
-    dz[1] = (float)(im * k);
+    dz[0] = (T)(re * k);
+    dz[1] = (T)(im * k);
   } else {
-    dz[s] = (float)gp;
+    dz[s] = (T)gp;
   }
 }
 
-__global__ void k_loss_finalize(LossArgs A) {
+template <typename T>
+__global__ void k_loss_finalize(LossArgsT<T> A) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= A.NI) return;
   const double* sm = A.sums + (int64_t)b * (A.S + 2);
@@ -212,22 +221,10 @@ int64_t loss_scratch_bytes(int NI, int h, int w, int C) {
   return (int64_t)sizeof(double) * (11 * tot + (int64_t)NI * (C + 2)) + 256;
 }
 
-int launch_loss(const float* img, const float* gt, int NI, int h, int w, int C, int sup,
-                double lam, float* dimg, double* stats, void* scratch, int64_t scratch_bytes,
-                cudaStream_t st) {
-  if (sup == 0 && C != 2) {
-    set_error("loss: magnitude supervision needs 2 channels, got %d", C);
-    return GSPARC_ERR_ARG;
-  }
-  if (h < 6 || w < 6) {
-    set_error("loss: image must be at least 6x6 for the 11-tap reflect window");
-    return GSPARC_ERR_ARG;
-  }
-  if (scratch_bytes < loss_scratch_bytes(NI, h, w, C)) {
-    set_error("loss: scratch too small");
-    return GSPARC_ERR_ARG;
-  }
-  LossArgs A;
+template <typename T>
+static int run_loss(const T* img, const T* gt, int NI, int h, int w, int C, int sup, double lam,
+                    T* dimg, double* stats, void* scratch, cudaStream_t st) {
+  LossArgsT<T> A;
   make_window(A.win);
   A.img = img;
   A.gt = gt;
@@ -249,12 +246,34 @@ int launch_loss(const float* img, const float* gt, int NI, int h, int w, int C, 
   if (cudaMemsetAsync(A.sums, 0, sizeof(double) * NI * (A.S + 2), st) != cudaSuccess)
     return check_launch("loss memset");
   const unsigned blocks = (unsigned)((tot + 255) / 256);
-  k_loss_h<<<blocks, 256, 0, st>>>(A);
-  k_loss_v<<<blocks, 256, 0, st>>>(A);
-  k_loss_adj_v<<<blocks, 256, 0, st>>>(A);
-  k_loss_adj_h<<<blocks, 256, 0, st>>>(A);
-  k_loss_finalize<<<(NI + 127) / 128, 128, 0, st>>>(A);
+  k_loss_h<T><<<blocks, 256, 0, st>>>(A);
+  k_loss_v<T><<<blocks, 256, 0, st>>>(A);
+  k_loss_adj_v<T><<<blocks, 256, 0, st>>>(A);
+  k_loss_adj_h<T><<<blocks, 256, 0, st>>>(A);
+  k_loss_finalize<T><<<(NI + 127) / 128, 128, 0, st>>>(A);
   return check_launch("k_loss");
+}
+
+int launch_loss(const void* img, const void* gt, int dtype, int NI, int h, int w, int C, int sup,
+                double lam, void* dimg, double* stats, void* scratch, int64_t scratch_bytes,
+                cudaStream_t st) {
+  if (sup == 0 && C != 2) {
+    set_error("loss: magnitude supervision needs 2 channels, got %d", C);
+    return GSPARC_ERR_ARG;
+  }
+  if (h < 6 || w < 6) {
+    set_error("loss: image must be at least 6x6 for the 11-tap reflect window");
+    return GSPARC_ERR_ARG;
+  }
+  if (scratch_bytes < loss_scratch_bytes(NI, h, w, C)) {
+    set_error("loss: scratch too small");
+    return GSPARC_ERR_ARG;
+  }
+  if (dtype == GSPARC_F64)
+    return run_loss<double>((const double*)img, (const double*)gt, NI, h, w, C, sup, lam,
+                            (double*)dimg, stats, scratch, st);
+  return run_loss<float>((const float*)img, (const float*)gt, NI, h, w, C, sup, lam,
+                         (float*)dimg, stats, scratch, st);
 }
 
 }  // namespace gs

@@ -177,7 +177,11 @@ static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   const size_t smem = sizeof(R) * ((size_t)CB * TILE_PX + (size_t)NB * TILE_PX + NB * CB + NB * 6) +
                       sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
   auto kern = k_raster_bwd<R, CB, NB>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attr_set = false;  // one per instantiation; keeps capture clean
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
   const int chunks = (int)((A.Cp + CB - 1) / CB);
   kern<<<dim3(ntiles, chunks), 256, smem, st>>>(A);
   return check_launch("k_raster_bwd");

@@ -208,21 +208,22 @@ def split_flat(flat, n, P):
 
 
 class LossWorkspace:
-    """Scratch + outputs for K7 (loss forward/backward)."""
+    """Scratch + outputs for K7 (loss forward/backward).  `dtype` of the
+    image / ground truth / dL tensors: torch.float32 or torch.float64."""
 
-    def __init__(self, n_img, h, w, C, device):
+    def __init__(self, n_img, h, w, C, device, dtype=torch.float32):
         nbytes = int(lib().gsparc_loss_scratch_bytes(n_img, h, w, C))
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
         self.stats = torch.zeros((n_img, 4), dtype=torch.float64, device=device)
-        self.dimg = torch.empty((n_img, h, w, C), dtype=torch.float32,
-                                device=device)
+        self.dimg = torch.empty((n_img, h, w, C), dtype=dtype, device=device)
+        self.dtype_code = _lib.F64 if dtype == torch.float64 else _lib.F32
         self.shape = (n_img, h, w, C)
 
     def run(self, img, gt, supervision, lam):
         n_img, h, w, C = self.shape
         check(lib().gsparc_loss_fwd_bwd(
             ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(gt.data_ptr()),
-            n_img, h, w, C, int(supervision), float(lam),
+            self.dtype_code, n_img, h, w, C, int(supervision), float(lam),
             ctypes.c_void_p(self.dimg.data_ptr()),
             ctypes.c_void_p(self.stats.data_ptr()),
             ctypes.c_void_p(self.scratch.data_ptr()), self.scratch.numel(),

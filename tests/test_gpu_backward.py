@@ -1,0 +1,150 @@
+"""GPU parity of the backward path (K5 raster backward + K6 per-Gaussian
+chain) against the real reference's gradients (golden fixtures), the CPU
+oracle and central finite differences.  Mirrors
+/root/reference/pkg/tests/test_rasterizer.py:157-212.
+
+Bar (north_star): per parameter group ||g_gpu - g_ref||_inf / ||g_ref||_inf
+<= 1e-4 for the fp32 path; 1e-9 for the f64 verification path."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, golden_cloud, golden_dL
+
+pytestmark = pytest.mark.gpu
+
+RX, W = np.zeros(3), np.eye(3)
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2511_22793_b200 import rasterizer
+    return rasterizer
+
+
+@pytest.fixture(scope="module")
+def pose():
+    from paper_2511_22793_b200 import ViewPose
+    return ViewPose(np.zeros(3))
+
+
+def host_cloud(oc):
+    from paper_2511_22793_b200 import GaussianCloud
+    return GaussianCloud(oc.positions, oc.log_scales, oc.rotations,
+                         oc.raw_opacities, oc.mlp_weights, oc.mlp_dims)
+
+
+def group_err(g, ref):
+    return {k: np.abs(np.asarray(g[k]) - ref[k]).max() /
+            max(np.abs(ref[k]).max(), 1e-30) for k in O.GROUPS}
+
+
+@pytest.mark.parametrize("case", ["rand96_0", "rand96_1", "rand96_2", "bwd4",
+                                  "bwd64", "bench512"])
+def test_backward_matches_golden(case, R, pose):
+    fx = golden(case)
+    cloud = host_cloud(golden_cloud(fx))
+    dt = np.dtype(str(fx["dtype"])).type
+    img, aux = R.rasterize_forward(cloud, pose, fx["tx"], int(fx["w"]),
+                                   int(fx["h"]), dtype=dt,
+                                   t_eps=float(fx["t_eps"]))
+    flips = int((aux.contrib_count != fx["count"]).sum())
+    if flips:
+        pytest.skip(f"{flips} forward threshold flips; gradient parity is "
+                    "checked on flip-free scenes")
+    g = R.rasterize_backward(golden_dL(fx), cloud, pose, fx["tx"], aux)
+    ref = {k: fx["grad_" + k] for k in O.GROUPS}
+    err = group_err(g.arrays(), ref)
+    tol = 1e-4 if dt == np.float32 else 1e-9
+    assert max(err.values()) <= tol, err
+    assert all(v.dtype == np.float64 for v in g.arrays().values())
+
+
+def test_finite_differences_f64(R, pose):
+    """tests/test_rasterizer.py:158-185 through the GPU f64 path."""
+    w, h = 24, 9
+    oc = O.perturbed_scene(4, seed=16)
+    cloud = host_cloud(oc)
+    tx = np.array([0.5, 0.2, -0.3])
+    rng = np.random.default_rng(17)
+    U = rng.normal(size=(h, w, 2))
+
+    def loss(c):
+        img, _ = R.rasterize_forward(c, pose, tx, w, h, dtype=np.float64)
+        return float(np.sum(U * img.data))
+
+    _, aux = R.rasterize_forward(cloud, pose, tx, w, h, dtype=np.float64)
+    grads = R.rasterize_backward(U, cloud, pose, tx, aux)
+    step = 1e-5
+    for name, arr in cloud.param_arrays().items():
+        g = grads.arrays()[name]
+        for fi in rng.choice(arr.size, size=min(20, arr.size), replace=False):
+            idx = np.unravel_index(fi, arr.shape)
+            cp, cm = cloud.copy(), cloud.copy()
+            cp.param_arrays()[name][idx] += step
+            cm.param_arrays()[name][idx] -= step
+            fd = (loss(cp) - loss(cm)) / (2 * step)
+            assert abs(g[idx] - fd) <= 1e-4 * max(1.0, abs(fd)), \
+                f"{name}{idx}: analytic {g[idx]:.3e} fd {fd:.3e}"
+
+
+@pytest.mark.parametrize("n,F", [(2000, 1), (800, 3)])
+def test_against_oracle(n, F, R, pose):
+    oc = O.round_f32(O.perturbed_scene(n, seed=3, F=F))
+    tx = O.sample_tx(11, 1)[0]
+    _, aux_ref = O.forward(oc, RX, W, tx, 180, 45)
+    U = np.random.default_rng(5).normal(size=(45, 180, 2 * F))
+    ref = O.backward(U, oc, tx, aux_ref)
+    img, aux = R.rasterize_forward(host_cloud(oc), pose, tx, 180, 45)
+    if (aux.contrib_count != aux_ref.contrib_count).any():
+        pytest.skip("forward threshold flip")
+    g = R.rasterize_backward(U, host_cloud(oc), pose, tx, aux)
+    err = group_err(g.arrays(), ref)
+    assert max(err.values()) <= 1e-4, err
+
+
+def test_batched_backward_is_sum_of_singles(R, pose):
+    import torch
+    from paper_2511_22793_b200 import DeviceCloud
+    from paper_2511_22793_b200.engine import split_flat
+    oc = O.round_f32(O.perturbed_scene(300, seed=4))
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    txs = O.sample_tx(3, 4)
+    U = np.random.default_rng(6).normal(size=(4, 45, 180, 2))
+    _, frame = R.rasterize_forward_batch(dc, pose, txs, 180, 45,
+                                         with_backward=True)
+    dL = torch.as_tensor(U, dtype=torch.float32, device="cuda")
+    flat = R.rasterize_backward_batch(dL, dc, pose, txs, frame)
+    got = {k: v.double().cpu().numpy()
+           for k, v in split_flat(flat, dc.n, dc.P).items()}
+    want = {k: 0.0 for k in O.GROUPS}
+    for b in range(4):
+        _, aux = R.rasterize_forward(dc, pose, txs[b], 180, 45)
+        g = R.rasterize_backward(U[b], dc, pose, txs[b], aux).arrays()
+        want = {k: want[k] + g[k] for k in O.GROUPS}
+    err = group_err(got, want)
+    assert max(err.values()) <= 1e-5, err
+
+
+def test_zero_upstream_and_aux_mismatch(R, pose):
+    oc = O.perturbed_scene(6, seed=19)
+    c = host_cloud(oc)
+    _, aux = R.rasterize_forward(c, pose, [0, 0, 0], 36, 9)
+    g = R.rasterize_backward(np.zeros((9, 36, 2)), c, pose, [0, 0, 0], aux)
+    for arr in g.arrays().values():
+        assert not arr.any()
+    other = host_cloud(O.perturbed_scene(5, seed=18))
+    with pytest.raises(ValueError):
+        R.rasterize_backward(np.zeros((9, 36, 2)), other, pose, [0, 0, 0], aux)
+    with pytest.raises(ValueError):
+        R.rasterize_backward(np.zeros((9, 36, 2)), c, pose, [1, 0, 0], aux)
+
+
+def test_check_finite(R):
+    oc = O.perturbed_scene(2, seed=20)
+    g = R.ParamGradients.zeros_like(host_cloud(oc))
+    g.check_finite()
+    g.positions[0, 0] = np.nan
+    with pytest.raises(FloatingPointError, match="positions"):
+        g.check_finite()
