@@ -297,7 +297,8 @@ def run_ours(args):
     e_s = torch.cuda.Event(enable_timing=True)
     e_e = torch.cuda.Event(enable_timing=True)
     for i in range(3):
-        pin_tx.copy_(torch.as_tensor(txs_np[i * B:(i + 1) * B]))
+        k = i % total_steps
+        pin_tx.copy_(torch.as_tensor(txs_np[k * B:(k + 1) * B]))
         out, _ = rasterize_forward_batch(dc, pose, pin_tx, w, h, lazy=lazy,
                                          frame=frame, image=img)
         pin_img.copy_(out, non_blocking=True)
@@ -366,7 +367,7 @@ def run_ours(args):
             line["cpu_baseline"] = {
                 "value": 1.0 / t, "unit": "renders/s", "cores": threads,
                 "kind": "port",
-                "sample": f"1 full render (same scene, TX {list(np.round(txs_np[0], 3))}) "
+                "sample": f"1 full render (same scene, TX {[round(float(v), 3) for v in txs_np[0]]}) "
                           "with the NumPy oracle, tile thread pool"}
     if dist:
         dist.barrier()

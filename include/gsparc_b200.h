@@ -107,7 +107,7 @@ typedef struct gsparc_frame_layout {
   int64_t off_tile_count; /* i32  [ntiles]                              */
   int64_t off_tile_cursor;/* i32  [ntiles]                              */
   int64_t off_tile_start; /* i32  [ntiles+1]                            */
-  int64_t off_tile_stop;  /* i32  [ntiles] list length actually visited */
+  int64_t off_tile_stop;  /* i32  [ntiles*4] list prefix visited per sub-tile */
   int64_t off_pairs;      /* u64  [pair_capacity] per-tile sorted lists */
   int64_t off_T;          /* dtype[h,w] final transmittance             */
   int64_t off_count;      /* i32  [h,w] contributor count               */

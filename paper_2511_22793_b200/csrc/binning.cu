@@ -137,13 +137,16 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs A) {
 // the next power of two never moves, so no padding is stored).
 template <bool SHARED>
 __device__ void bitonic_sort(uint64_t* a, int n) {
-  int np2 = 1;
-  while (np2 < n) np2 <<= 1;
-  for (int k = 2; k <= np2; k <<= 1) {
+  int np2 = 1, lg = 0;
+  while (np2 < n) {
+    np2 <<= 1;
+    ++lg;
+  }
+  for (int lk = 1; lk <= lg; ++lk) {
+    const int k = 1 << lk;
     // first step of the merge: compare i with its mirror in the k-block
     for (int p = threadIdx.x; p < np2 / 2; p += blockDim.x) {
-      int half = k >> 1;
-      int blk = p / half, off = p % half;
+      const int blk = p >> (lk - 1), off = p & ((k >> 1) - 1);
       int i = blk * k + off;
       int j = blk * k + (k - 1 - off);
       if (j < n) {
@@ -155,10 +158,11 @@ __device__ void bitonic_sort(uint64_t* a, int n) {
       }
     }
     __syncthreads();
-    for (int s = k >> 2; s > 0; s >>= 1) {
+    for (int ls = lk - 2; ls >= 0; --ls) {
+      const int s = 1 << ls;
       for (int p = threadIdx.x; p < np2 / 2; p += blockDim.x) {
-        int blk = p / s, off = p % s;
-        int i = blk * 2 * s + off;
+        const int blk = p >> ls, off = p & (s - 1);
+        int i = (blk << (ls + 1)) + off;
         int j = i + s;
         if (j < n) {
           uint64_t x = a[i], y = a[j];

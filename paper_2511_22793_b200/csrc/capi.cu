@@ -130,7 +130,7 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_tile_count = take(sizeof(int) * L.ntiles);
   L.off_tile_cursor = take(sizeof(int) * L.ntiles);
   L.off_tile_start = take(sizeof(int) * (L.ntiles + 1));
-  L.off_tile_stop = take(sizeof(int) * L.ntiles);
+  L.off_tile_stop = take(sizeof(int) * L.ntiles * 4);  // per sub-tile
   L.off_pairs = take(8 * pair_capacity);
   L.off_T = take(esz * px);
   L.off_count = take(sizeof(int) * px);

@@ -99,31 +99,46 @@ struct AlphaOut {
   R alpha, raw, g, dx, dy;
 };
 
+// exp for the f32 raster: 2^(x log2 e) with the product error carried
+// (t + e = x log2 e exactly to ~2^-48) and one ex2.approx; ~2 ulp, branch
+// free.  numpy's own f32 exp is not correctly rounded either (SURVEY.md 0
+// item 5), so alpha parity is tolerance based and threshold flips are
+// counted by the tests.
+__device__ __forceinline__ float exp_f32(float x) {
+  const float L2E_HI = 1.44269502162933349609375f;
+  const float L2E_LO = 1.925963033500011e-08f;
+  const float t = __fmul_rn(x, L2E_HI);
+  const float e = __fmaf_rn(x, L2E_HI, -t) + x * L2E_LO;
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+  return __fmaf_rn(r, e * 0.693147180559945309f, r);
+}
+
+// Per-pixel alpha in the exact operation order of rasterizer.py:177-183.
+// Domain: mx in [0, w] (equirect azimuth) and pcx in (0, w), so
+// t = (pcx - mx) + w/2 lies in (-w/2, 3w/2) and numpy's float remainder
+// reduces to one conditional +-w (t - w is exact by Sterbenz; t + w rounds
+// exactly like numpy's fmod-then-add).  Branch free.
 template <typename R>
 __device__ __forceinline__ AlphaOut<R> pixel_alpha(R pcx, R pcy, R mx, R my, R ca,
                                                   R cb, R cc, R op, R w, R half_w) {
   AlphaOut<R> o;
-  R t = add(sub(pcx, mx), half_w);
-  // fast exact remainder for t in [-w, 2w); general fallback otherwise
-  R m;
-  if (t >= R(0) && t < w) {
-    m = t;
-  } else if (t >= w && t < R(2) * w) {
-    m = sub(t, w);  // exact (Sterbenz)
-  } else if (t < R(0) && t > -w) {
-    m = add(t, w);  // numpy: fmod(t,w)=t, then t+w rounded
-  } else {
-    m = py_mod<R>(t, w);
-  }
+  const R t = add(sub(pcx, mx), half_w);
+  R m = t >= w ? sub(t, w) : t;
+  m = t < R(0) ? add(t, w) : m;
   o.dx = sub(m, half_w);
   o.dy = sub(pcy, my);
-  R q = add(add(mul(mul(ca, o.dx), o.dx), mul(mul(mul(R(2), cb), o.dx), o.dy)),
-            mul(mul(cc, o.dy), o.dy));
-  o.g = exp_r(mul(R(-0.5), q));
+  const R q = add(add(mul(mul(ca, o.dx), o.dx), mul(mul(mul(R(2), cb), o.dx), o.dy)),
+                  mul(mul(cc, o.dy), o.dy));
+  if constexpr (sizeof(R) == 4) {
+    o.g = exp_f32(mul(R(-0.5), q));
+  } else {
+    o.g = exp(mul(R(-0.5), q));
+  }
   o.raw = mul(op, o.g);
-  R amax = sizeof(R) == 4 ? R(ALPHA_MAX_F) : R(ALPHA_MAX);
-  R amin = sizeof(R) == 4 ? R(ALPHA_MIN_F) : R(ALPHA_MIN);
-  R a = o.raw < amax ? o.raw : amax;  // np.minimum (NaN-free inputs)
+  const R amax = sizeof(R) == 4 ? R(ALPHA_MAX_F) : R(ALPHA_MAX);
+  const R amin = sizeof(R) == 4 ? R(ALPHA_MIN_F) : R(ALPHA_MIN);
+  const R a = o.raw < amax ? o.raw : amax;  // np.minimum (NaN-free inputs)
   o.alpha = (a < amin) ? R(0) : a;
   return o;
 }

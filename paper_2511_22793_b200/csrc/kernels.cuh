@@ -5,6 +5,7 @@
 namespace gs {
 
 GeoConst make_geo_const(int w, int h);
+int forward_sub_rows(const gsparc_frame_layout& L, int64_t Cp);
 
 int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
                       const gsparc_frame_layout& L, char* frame, cudaStream_t st);

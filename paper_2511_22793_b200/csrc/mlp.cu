@@ -101,13 +101,7 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
 }
 
 // Wide head, f32 weights, H == 16, I == 5, C % 4 == 0.
-__global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
-  if (gi >= count) return;
-  const int64_t i = A.live_list ? A.live_list[gi] : gi;
-  if (!A.live_list && A.key[i] == ~0ULL) return;
+__device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int lane) {
   const float4 r1 = A.rec32[2 * i + 1];
   const float* w = A.w32 + i * (int64_t)A.P;
   const int C = A.C;
@@ -146,6 +140,18 @@ __global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
         out[o] = (float)((double)(part + __ldg(b2 + o)) / d);
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < count;
+       gi += nwarps) {
+    const int64_t i = A.live_list ? A.live_list[gi] : gi;
+    if (!A.live_list && A.key[i] == ~0ULL) continue;
+    mlp_wide_one(A, i, lane);
   }
 }
 
@@ -189,7 +195,9 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     k_mlp_narrow<double><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
   } else if (A.C % 4 == 0 && A.C >= 16 && A.H == 16 && A.I == 5) {
     int64_t threads = cloud.n * 32;
-    k_mlp_wide<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
+    int64_t blocks = (threads + 255) / 256;
+    if (live_only && blocks > 148 * 8) blocks = 148 * 8;  // grid-stride over the live list
+    k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
   } else {
     int64_t threads = cloud.n * B;
     k_mlp_narrow<float><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);

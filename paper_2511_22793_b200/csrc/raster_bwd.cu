@@ -23,7 +23,7 @@ namespace gs {
 struct BwdArgs {
   const uint64_t* pairs;
   const int* tile_start;
-  const int* tile_stop;
+  const int* sub_stop;  // per sub-tile (same split as the forward AUX pass)
   const float4* rec32;
   const double* rec64;
   const void* coef;
@@ -35,28 +35,31 @@ struct BwdArgs {
   const int* counters;
   int64_t Cp;
   int C;
-  int w, h, ntx;
+  int w, h, ntx, sr, nsub;
 };
 
 template <typename R, int CB, int NB>
 __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  R* s_u = (R*)smraw;                    // [CB][256]
-  R* s_wgt = s_u + CB * TILE_PX;         // [NB][256]
-  R* s_coef = s_wgt + NB * TILE_PX;      // [NB][CB]
+  const int P = blockDim.x;              // pixels of this sub-tile
+  R* s_u = (R*)smraw;                    // [CB][P]
+  R* s_wgt = s_u + CB * P;               // [NB][P]
+  R* s_coef = s_wgt + NB * P;            // [NB][CB]
   R* s_red = s_coef + NB * CB;           // [NB][6]
   Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6);  // [NB]
   int* s_idx = (int*)(s_rec + NB);       // [NB]
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
-  const int tile = blockIdx.x, chunk = blockIdx.y;
+  const int sidx = blockIdx.x, chunk = blockIdx.y;
+  const int tile = sidx / A.nsub, part = sidx - tile * A.nsub;
   const int tid = threadIdx.x, pix = tid;
   const int lane = tid & 31;
   const int tx_ = tile % A.ntx, ty = tile / A.ntx;
-  const int px = tx_ * TILE + (pix & (TILE - 1)), py = ty * TILE + pix / TILE;
+  const int px = tx_ * TILE + (pix & (TILE - 1));
+  const int py = ty * TILE + part * A.sr + pix / TILE;
   const bool inside = px < A.w && py < A.h;
   const int start = A.tile_start[tile];
-  const int nvisit = A.tile_stop[tile];
+  const int nvisit = A.sub_stop[sidx];
   if (nvisit == 0) return;
   const int chunk_base = chunk * CB;
   const R pcx = (R)px + R(0.5), pcy = (R)py + R(0.5);
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       v = dL[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch];
     }
     u[c] = v;
-    s_u[c * TILE_PX + pix] = v;
+    s_u[c * P + pix] = v;
   }
   const int p = py * A.w + px;
   R T = inside ? ((const R*)A.T_final)[p] : R(1);
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
           }
         }
       }
-      s_wgt[j * TILE_PX + pix] = wgt;
+      s_wgt[j * P + pix] = wgt;
       const bool any = __any_sync(0xffffffffu, g_sig != R(0) || gc0 != R(0) || gc2 != R(0) ||
                                                    gm0 != R(0) || gm1 != R(0));
       if (any) {
@@ -158,11 +161,11 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       const int j = o / CB, c = o - j * CB;
       const int64_t cc = chunk_base + c;
       if (cc >= A.Cp) continue;
-      const R* wr = s_wgt + j * TILE_PX;
-      const R* ur = s_u + c * TILE_PX;
+      const R* wr = s_wgt + j * P;
+      const R* ur = s_u + c * P;
       R s = R(0);
 #pragma unroll 8
-      for (int q = 0; q < TILE_PX; ++q) s += wr[q] * ur[q];
+      for (int q = 0; q < P; ++q) s += wr[q] * ur[q];
       if (s != R(0)) atomicAdd(gcoef + (int64_t)s_idx[j] * A.Cp + cc, s);
     }
     for (int o = tid; o < nb * 6; o += blockDim.x) {
@@ -174,16 +177,19 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
 
 template <typename R, int CB, int NB>
 static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
-  const size_t smem = sizeof(R) * ((size_t)CB * TILE_PX + (size_t)NB * TILE_PX + NB * CB + NB * 6) +
+  const int P = TILE * A.sr;
+  const size_t smem_max = sizeof(R) * ((size_t)CB * 256 + (size_t)NB * 256 + NB * CB + NB * 6) +
+                          sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
+  const size_t smem = sizeof(R) * ((size_t)CB * P + (size_t)NB * P + NB * CB + NB * 6) +
                       sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
   auto kern = k_raster_bwd<R, CB, NB>;
   static bool attr_set = false;  // one per instantiation; keeps capture clean
   if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     attr_set = true;
   }
   const int chunks = (int)((A.Cp + CB - 1) / CB);
-  kern<<<dim3(ntiles, chunks), 256, smem, st>>>(A);
+  kern<<<dim3(ntiles * A.nsub, chunks), P, smem, st>>>(A);
   return check_launch("k_raster_bwd");
 }
 
@@ -192,7 +198,7 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   BwdArgs A;
   A.pairs = (const uint64_t*)(frame + L.off_pairs);
   A.tile_start = (const int*)(frame + L.off_tile_start);
-  A.tile_stop = (const int*)(frame + L.off_tile_stop);
+  A.sub_stop = (const int*)(frame + L.off_tile_stop);
   A.rec32 = (const float4*)(frame + L.off_rec32);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.coef = frame + L.off_coef;
@@ -207,6 +213,8 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.w = L.width;
   A.h = L.height;
   A.ntx = L.ntx;
+  A.sr = forward_sub_rows(L, A.Cp);
+  A.nsub = TILE / A.sr;
   const size_t esz = L.dtype == GSPARC_F64 ? 8 : 4;
   if (cudaMemsetAsync(A.gcoef, 0, esz * (size_t)L.n * (size_t)L.channels, st) != cudaSuccess ||
       cudaMemsetAsync(A.ggeo, 0, esz * (size_t)L.n * 8, st) != cudaSuccess)
