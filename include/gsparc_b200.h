@@ -117,6 +117,10 @@ typedef struct gsparc_frame_layout {
   int64_t off_coef;       /* f32/f64 [n,channels] s/d per Gaussian,TX   */
   int64_t off_gcoef;      /* f32/f64 [n,channels] dL/dcoef (backward)   */
   int64_t off_ggeo;       /* f32/f64 [n,8] dL/d(conic3,mean2d2,sigma)   */
+  int64_t off_pair_rec;   /* f32  [pair_capacity,8] raster record per list
+                             entry (f32 frames), list order               */
+  int64_t off_wstop;      /* i32  [ntiles*8] visited list prefix per
+                             32-pixel warp (2 rows x 16 px)               */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

@@ -40,7 +40,7 @@ class CView(ctypes.Structure):
 _LAYOUT_OFFSETS = ("key", "rec32", "rec64", "rect", "counters", "tile_count",
                    "tile_cursor", "tile_start", "tile_stop", "pairs", "T",
                    "count", "last", "live", "live_list", "coef", "gcoef",
-                   "ggeo")
+                   "ggeo", "pair_rec", "wstop")
 
 
 class CLayout(ctypes.Structure):

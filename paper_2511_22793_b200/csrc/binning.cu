@@ -206,29 +206,124 @@ __device__ void fix_coarse_ties(uint64_t* a, int n, const uint64_t* key) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_tile_sort(uint64_t* pairs, const int* tile_start,
-                                                    const uint64_t* key, int* counters, int cap) {
-  extern __shared__ uint64_t s_pairs[];
-  if (counters[GSPARC_CNT_OVERFLOW]) return;
-  const int t = blockIdx.x;
-  const int s = tile_start[t], n = tile_start[t + 1] - s;
-  if (n <= 1) return;
-  uint64_t* g = pairs + s;
-  if (n <= cap) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) s_pairs[j] = g[j];
-    __syncthreads();
-    bitonic_sort<true>(s_pairs, n);
-    fix_coarse_ties(s_pairs, n, key);
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = s_pairs[j];
-  } else {
-    if (threadIdx.x == 0) atomicAdd(counters + GSPARC_CNT_BIGTILE, 1);
-    bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
-    fix_coarse_ties(g, n, key);
+// Register bitonic sort of up to 8192 keys per CTA (1024 threads x 8 keys,
+// blocked layout i = 8*tid + e).  Compare-exchange partners at index
+// distance < 8 are in the same thread, < 256 in the same warp (shuffles),
+// larger go through shared memory.  All comparators put the minimum at the
+// lower index (ascending-only network), so the virtual +inf padding never
+// moves and is never stored.
+constexpr int RB_E = 8;
+constexpr int RB_T = 1024;
+constexpr int RB_CAP = RB_E * RB_T;
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// in-thread compare-exchange of x[e] with x[e ^ D] (D compile time)
+template <int D>
+__device__ __forceinline__ void cx_local(uint64_t (&x)[RB_E]) {
+#pragma unroll
+  for (int e = 0; e < RB_E; ++e) {
+    if ((e ^ D) > e) {
+      const uint64_t a = x[e], b = x[e ^ D];
+      x[e] = a < b ? a : b;
+      x[e ^ D] = a < b ? b : a;
+    }
   }
 }
 
-constexpr int SORT_SMEM_CAP = 16384;  // 128 KiB of u64 per tile in smem
+// cross-thread step: partner thread t ^ tm; MIRROR pairs element e with the
+// partner's 7 - e (first merge step), otherwise with the partner's e.
+template <bool MIRROR>
+__device__ __forceinline__ void cx_remote(uint64_t (&x)[RB_E], uint64_t* sm, int tm,
+                                          bool lo_half) {
+  const int t = threadIdx.x;
+  uint64_t y[RB_E];
+  if (tm < 32) {
+#pragma unroll
+    for (int e = 0; e < RB_E; ++e) y[e] = shfl64(x[MIRROR ? RB_E - 1 - e : e], (t & 31) ^ tm);
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < RB_E; ++e) sm[t * RB_E + e] = x[e];
+    __syncthreads();
+    const int pt = t ^ tm;
+#pragma unroll
+    for (int e = 0; e < RB_E; ++e) y[e] = sm[pt * RB_E + (MIRROR ? RB_E - 1 - e : e)];
+  }
+#pragma unroll
+  for (int e = 0; e < RB_E; ++e) {
+    const uint64_t a = x[e], b = y[e];
+    x[e] = lo_half ? (a < b ? a : b) : (a < b ? b : a);
+  }
+}
+
+__device__ void reg_bitonic(uint64_t (&x)[RB_E], uint64_t* sm, int np2) {
+  const int t = threadIdx.x;
+  // k = 2, 4, 8: entirely inside the thread (mirror + cleaners)
+  cx_local<1>(x);
+  cx_local<3>(x);
+  cx_local<1>(x);
+  cx_local<7>(x);
+  cx_local<2>(x);
+  cx_local<1>(x);
+  for (int k = 16; k <= np2; k <<= 1) {
+    cx_remote<true>(x, sm, (k - 1) >> 3, (t & (k >> 4)) == 0);
+    for (int s = k >> 2; s >= RB_E; s >>= 1) cx_remote<false>(x, sm, s >> 3, (t & (s >> 3)) == 0);
+    cx_local<4>(x);
+    cx_local<2>(x);
+    cx_local<1>(x);
+  }
+}
+
+// Sort each tile's bucket by (coarse depth, index), fix coarse ties by the
+// full f64 key, then stage the f32 raster record of every entry in list
+// order (pair_rec) so the raster streams records instead of gathering them.
+__global__ void __launch_bounds__(RB_T) k_tile_sort(uint64_t* pairs, const int* tile_start,
+                                                    const uint64_t* key, int* counters,
+                                                    const float4* rec32, float4* pair_rec) {
+  extern __shared__ uint64_t s_pairs[];  // RB_CAP entries
+  if (counters[GSPARC_CNT_OVERFLOW]) return;
+  const int t = blockIdx.x;
+  const int s = tile_start[t], n = tile_start[t + 1] - s;
+  uint64_t* g = pairs + s;
+  if (n > 1 && n <= RB_CAP) {
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    uint64_t x[RB_E];
+#pragma unroll
+    for (int e = 0; e < RB_E; ++e) {
+      const int i = threadIdx.x * RB_E + e;
+      x[e] = i < n ? g[i] : ~0ULL;
+    }
+    reg_bitonic(x, s_pairs, np2 < RB_E ? RB_E : np2);
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < RB_E; ++e) s_pairs[threadIdx.x * RB_E + e] = x[e];
+    __syncthreads();
+    fix_coarse_ties(s_pairs, n, key);
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = s_pairs[j];
+  } else if (n > RB_CAP) {
+    if (threadIdx.x == 0) atomicAdd(counters + GSPARC_CNT_BIGTILE, 1);
+    bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
+    fix_coarse_ties(g, n, key);
+    __syncthreads();
+  }
+  if (pair_rec) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint32_t idx = (uint32_t)g[j];
+      const float4 a = __ldg(rec32 + 2 * idx), b = __ldg(rec32 + 2 * idx + 1);
+      pair_rec[2 * (size_t)(s + j)] = a;
+      pair_rec[2 * (size_t)(s + j) + 1] = make_float4(b.x, b.y, __int_as_float((int)idx), 0.f);
+    }
+  }
+}
+
 
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
   BinArgs A;
@@ -253,11 +348,12 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SORT_SMEM_CAP * (int)sizeof(uint64_t));
+                         RB_CAP * (int)sizeof(uint64_t));
     attr_set = true;
   }
-  k_tile_sort<<<L.ntiles, 1024, SORT_SMEM_CAP * sizeof(uint64_t), st>>>(
-      A.pairs, A.tile_start, A.key, A.counters, SORT_SMEM_CAP);
+  float4* pair_rec = L.dtype == GSPARC_F64 ? nullptr : (float4*)(frame + L.off_pair_rec);
+  k_tile_sort<<<L.ntiles, RB_T, RB_CAP * sizeof(uint64_t), st>>>(
+      A.pairs, A.tile_start, A.key, A.counters, (const float4*)(frame + L.off_rec32), pair_rec);
   return check_launch("k_tile_sort");
 }
 

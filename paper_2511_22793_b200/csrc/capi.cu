@@ -140,6 +140,8 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_coef = take(esz * nn * channels);
   L.off_gcoef = with_backward ? take(esz * nn * channels) : 0;
   L.off_ggeo = with_backward ? take(esz * nn * 8) : 0;
+  L.off_pair_rec = dtype == GSPARC_F32 ? take(32 * pair_capacity) : 0;
+  L.off_wstop = take(sizeof(int) * L.ntiles * 8);
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

@@ -23,7 +23,7 @@ namespace gs {
 struct BwdArgs {
   const uint64_t* pairs;
   const int* tile_start;
-  const int* sub_stop;  // per sub-tile (same split as the forward AUX pass)
+  const int* wstop;  // visited prefix per 32-pixel warp (forward AUX pass)
   const float4* rec32;
   const double* rec64;
   const void* coef;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   const int py = ty * TILE + part * A.sr + pix / TILE;
   const bool inside = px < A.w && py < A.h;
   const int start = A.tile_start[tile];
-  const int nvisit = A.sub_stop[sidx];
+  const int nvisit = max(A.wstop[tile * 8 + part * 2], A.wstop[tile * 8 + part * 2 + 1]);
   if (nvisit == 0) return;
   const int chunk_base = chunk * CB;
   const R pcx = (R)px + R(0.5), pcy = (R)py + R(0.5);
@@ -198,7 +198,7 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   BwdArgs A;
   A.pairs = (const uint64_t*)(frame + L.off_pairs);
   A.tile_start = (const int*)(frame + L.off_tile_start);
-  A.sub_stop = (const int*)(frame + L.off_tile_stop);
+  A.wstop = (const int*)(frame + L.off_wstop);
   A.rec32 = (const float4*)(frame + L.off_rec32);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.coef = frame + L.off_coef;
