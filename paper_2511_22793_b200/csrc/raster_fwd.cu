@@ -373,6 +373,9 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
               (long long)L.channels);
     return GSPARC_ERR_ARG;
   }
+  // lazy two-pass path for wide channels: tensor-core accumulation
+  if (L.dtype == GSPARC_F32 && A.Cp > 4 && pass != 0)
+    return launch_raster_tc(L, frame, n_tx, C, t_eps, pass, img, st);
   if (pass != 2) {
     if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
       return check_launch("raster live memset");
