@@ -279,35 +279,129 @@ __device__ void reg_bitonic(uint64_t (&x)[RB_E], uint64_t* sm, int np2) {
   }
 }
 
+// Block LSD radix sort of one tile's packed keys (coarse_depth32 << 32 |
+// index) in shared memory: 8-bit digits over the index bits actually used and
+// the 32 coarse-depth bits.  Keys are ranked warp by warp in list order
+// (warp-striped: key i = 256 w + 32 e + lane) with ballot-derived peers, so
+// every pass is stable and the result is the exact u64 order.  Cost O(n) per
+// pass, against O(n log^2 n) for the bitonic network it replaces.
+constexpr int RS_T = 1024;
+constexpr int RS_W = RS_T / 32;
+constexpr int RS_E = 8;
+constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
+
+__device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, int idx_bits) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int shifts[8];
+  int np = 0;
+  for (int b = 0; b < idx_bits; b += 8) shifts[np++] = b;
+  for (int b = 32; b < 64; b += 8) shifts[np++] = b;
+  for (int pass = 0; pass < np; ++pass) {
+    const int sh = shifts[pass];
+    int* wc = cnt + warp * 256;
+    for (int d = lane; d < 256; d += 32) wc[d] = 0;
+    __syncwarp();
+    int rank[RS_E];
+    int dig[RS_E];
+    const int wbase = warp * 32 * RS_E;
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int i = wbase + e * 32 + lane;
+      const bool valid = i < n;
+      const int d = valid ? (int)((src[valid ? i : 0] >> sh) & 0xFF) : 0;
+      // peers with the same 8-bit digit: AND of 8 bit-plane ballots
+      unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const unsigned m = __ballot_sync(0xffffffffu, (d >> b) & 1);
+        peers &= ((d >> b) & 1) ? m : ~m;
+      }
+      if (!valid) peers = 1u << lane;
+      const int leader = __ffs(peers) - 1;
+      int old = 0;
+      if (valid && lane == leader) {
+        old = wc[d];
+        wc[d] = old + __popc(peers);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rank[e] = old + __popc(peers & lt);
+      dig[e] = d;
+    }
+    __syncthreads();
+    // offsets: digit-major, warp-minor
+    if (tid < 256) {
+      int run = 0;
+      for (int w = 0; w < RS_W; ++w) {
+        const int c = cnt[w * 256 + tid];
+        cnt[w * 256 + tid] = run;
+        run += c;
+      }
+      cnt[RS_W * 256 + tid] = run;  // digit total
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 256 digit totals (8 per lane)
+      int loc[8];
+      int sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        loc[k] = sum;
+        sum += cnt[RS_W * 256 + tid * 8 + k];
+      }
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const int ex = inc - sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cnt[RS_W * 256 + 256 + tid * 8 + k] = ex + loc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int i = wbase + e * 32 + lane;
+      if (i < n) {
+        const int d = dig[e];
+        dst[cnt[RS_W * 256 + 256 + d] + cnt[warp * 256 + d] + rank[e]] = src[i];
+      }
+    }
+    __syncthreads();
+    uint64_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  // result is in `src` after the loop swap; copy back if needed
+  if (np & 1) {
+    for (int i = tid; i < n; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
+}
+
 // Sort each tile's bucket by (coarse depth, index), fix coarse ties by the
 // full f64 key, then stage the f32 raster record of every entry in list
 // order (pair_rec) so the raster streams records instead of gathering them.
-__global__ void __launch_bounds__(RB_T) k_tile_sort(uint64_t* pairs, const int* tile_start,
+__global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* tile_start,
                                                     const uint64_t* key, int* counters,
-                                                    const float4* rec32, float4* pair_rec) {
-  extern __shared__ uint64_t s_pairs[];  // RB_CAP entries
+                                                    const float4* rec32, float4* pair_rec,
+                                                    int idx_bits) {
+  extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
   if (counters[GSPARC_CNT_OVERFLOW]) return;
   const int t = blockIdx.x;
   const int s = tile_start[t], n = tile_start[t + 1] - s;
   uint64_t* g = pairs + s;
-  if (n > 1 && n <= RB_CAP) {
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    uint64_t x[RB_E];
-#pragma unroll
-    for (int e = 0; e < RB_E; ++e) {
-      const int i = threadIdx.x * RB_E + e;
-      x[e] = i < n ? g[i] : ~0ULL;
-    }
-    reg_bitonic(x, s_pairs, np2 < RB_E ? RB_E : np2);
+  if (n > 1 && n <= RS_CAP) {
+    uint64_t* a = s_keys;
+    uint64_t* b = s_keys + RS_CAP;
+    int* cnt = (int*)(s_keys + 2 * RS_CAP);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) a[j] = g[j];
     __syncthreads();
-#pragma unroll
-    for (int e = 0; e < RB_E; ++e) s_pairs[threadIdx.x * RB_E + e] = x[e];
+    block_radix_sort(a, b, cnt, n, idx_bits);
+    fix_coarse_ties(a, n, key);
     __syncthreads();
-    fix_coarse_ties(s_pairs, n, key);
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = s_pairs[j];
-  } else if (n > RB_CAP) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = a[j];
+  } else if (n > RS_CAP) {
     if (threadIdx.x == 0) atomicAdd(counters + GSPARC_CNT_BIGTILE, 1);
     bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
     fix_coarse_ties(g, n, key);
@@ -317,13 +411,12 @@ __global__ void __launch_bounds__(RB_T) k_tile_sort(uint64_t* pairs, const int* 
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const uint32_t idx = (uint32_t)g[j];
-      const float4 a = __ldg(rec32 + 2 * idx), b = __ldg(rec32 + 2 * idx + 1);
-      pair_rec[2 * (size_t)(s + j)] = a;
-      pair_rec[2 * (size_t)(s + j) + 1] = make_float4(b.x, b.y, __int_as_float((int)idx), 0.f);
+      const float4 a4 = __ldg(rec32 + 2 * idx), b4 = __ldg(rec32 + 2 * idx + 1);
+      pair_rec[2 * (size_t)(s + j)] = a4;
+      pair_rec[2 * (size_t)(s + j) + 1] = make_float4(b4.x, b4.y, __int_as_float((int)idx), 0.f);
     }
   }
 }
-
 
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
   BinArgs A;
@@ -345,15 +438,18 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   size_t smem = sizeof(int) * (3 * (size_t)L.ntiles + 1 + 40);
   k_bin<<<blocks, 256, smem, st>>>(A);
   GS_TRY(check_launch("k_bin"));
+  const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * (RS_W * 256 + 512);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         RB_CAP * (int)sizeof(uint64_t));
+    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
     attr_set = true;
   }
+  int idx_bits = 8;
+  while (idx_bits < 32 && ((int64_t)1 << idx_bits) < L.n) idx_bits += 8;
   float4* pair_rec = L.dtype == GSPARC_F64 ? nullptr : (float4*)(frame + L.off_pair_rec);
-  k_tile_sort<<<L.ntiles, RB_T, RB_CAP * sizeof(uint64_t), st>>>(
-      A.pairs, A.tile_start, A.key, A.counters, (const float4*)(frame + L.off_rec32), pair_rec);
+  k_tile_sort<<<L.ntiles, RS_T, smem_sort, st>>>(A.pairs, A.tile_start, A.key, A.counters,
+                                           (const float4*)(frame + L.off_rec32), pair_rec,
+                                           idx_bits);
   return check_launch("k_tile_sort");
 }
 

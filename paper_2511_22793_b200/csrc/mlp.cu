@@ -130,14 +130,26 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
     float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
     const double d = tx_distance(p, txb);
     float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
-    for (int f = lane; f < nvec; f += 32) {
-      float4 v = __ldg(w2v + f);
-      float part = v.x * h0 + v.y * h1 + v.z * h2 + v.w * h3;
-      part += __shfl_xor_sync(0xffffffffu, part, 1);
-      part += __shfl_xor_sync(0xffffffffu, part, 2);
-      if (q == 0) {
-        int o = f >> 2;
-        out[o] = (float)((double)(part + __ldg(b2 + o)) / d);
+    // issue every W2 load of this lane before using any (latency overlap)
+    constexpr int MAXV = 16;  // 4C/32 float4 per lane, C <= 128 per pass
+    for (int f0 = 0; f0 < nvec; f0 += 32 * MAXV) {
+      float4 v[MAXV];
+#pragma unroll
+      for (int u = 0; u < MAXV; ++u) {
+        const int f = f0 + u * 32 + lane;
+        v[u] = f < nvec ? __ldg(w2v + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < MAXV; ++u) {
+        const int f = f0 + u * 32 + lane;
+        if (f0 + u * 32 >= nvec) break;
+        float part = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        if (q == 0 && f < nvec) {
+          const int o = f >> 2;
+          out[o] = (float)((double)(part + __ldg(b2 + o)) / d);
+        }
       }
     }
   }

@@ -30,7 +30,7 @@ __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, doub
 
 __device__ __forceinline__ double np_floor_div16(double v) { return floor(v / 16.0); }
 
-__global__ void __launch_bounds__(256) k_preprocess(PrepArgs A) {
+__global__ void __launch_bounds__(128) k_preprocess(PrepArgs A) {
   extern __shared__ int s_tiles[];  // per-CTA tile histogram
   const int ntiles = A.gc.ntx * A.gc.nty;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
@@ -256,9 +256,9 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
       cudaMemsetAsync(frame + L.off_tile_count, 0, sizeof(int) * L.ntiles, st) != cudaSuccess)
     return check_launch("preprocess memset");
   if (cloud.n > 0) {
-    int blocks = (int)((cloud.n + 255) / 256);
+    int blocks = (int)((cloud.n + 127) / 128);
     size_t smem = sizeof(int) * (size_t)L.ntiles;
-    k_preprocess<<<blocks, 256, smem, st>>>(A);
+    k_preprocess<<<blocks, 128, smem, st>>>(A);
   }
   return check_launch("k_preprocess");
 }

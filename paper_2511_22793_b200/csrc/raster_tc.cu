@@ -55,7 +55,10 @@ struct PixState {
 __device__ __forceinline__ float chunk_weight(const float4* s_rec, int nvalid, int lane, float pcx,
                                               float pcy, float wR, float half_w, float teps,
                                               int list_pos0, PixState& st, bool& inc_out) {
-  const bool valid = lane < nvalid;
+  // a finished pixel sees no valid entries (branch free, so two pixels'
+  // chains interleave); its state is left untouched
+  const bool live_px = !st.done;
+  const bool valid = lane < nvalid && live_px;
   float a = 0.f;
   if (valid) {
     const float4 r0 = s_rec[2 * lane], r1 = s_rec[2 * lane + 1];
@@ -78,11 +81,11 @@ __device__ __forceinline__ float chunk_weight(const float4* s_rec, int nvalid, i
     st.cnt += __popc(incm);
     st.last = list_pos0 + (31 - __clz(incm)) + 1;
   }
-  if (first < 32) {
-    st.T = __shfl_sync(0xffffffffu, Tb, first);
-    st.done = true;
-  } else {
-    st.T = __shfl_sync(0xffffffffu, mul(st.T, P), 31);
+  const float Tfirst = __shfl_sync(0xffffffffu, Tb, first & 31);
+  const float Tall = __shfl_sync(0xffffffffu, mul(st.T, P), 31);
+  if (live_px) {
+    st.T = first < 32 ? Tfirst : Tall;
+    st.done = first < 32;
   }
   inc_out = inc;
   return inc ? mul(Tb, a) : 0.f;
@@ -124,24 +127,32 @@ __global__ void __launch_bounds__(512) k_raster_a(TcArgs A) {
     if (tid < SUP) s_live[tid] = 0;
     __syncthreads();
 #pragma unroll 1
-    for (int s = 0; s < TC_P / TC_WARPS; ++s) {
-      const int p = warp + TC_WARPS * s;
-      if (s_done[p]) continue;
-      int px, py;
-      pixel_xy(tile, half, p, A.ntx, px, py);
-      const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
-      PixState st{s_T[p], s_cnt[p], s_last[p], false};
-      for (int k0 = 0; k0 < nsup && !st.done; k0 += TC_K) {
-        bool inc;
-        chunk_weight(s_rec + 2 * k0, min(TC_K, nsup - k0), lane, pcx, pcy, wR, half_w, teps,
-                     cb - start + k0, st, inc);
-        if (inc) s_live[k0 + lane] = 1;
+    for (int s = 0; s < TC_P / TC_WARPS; s += 2) {
+      const int p0 = warp + TC_WARPS * s, p1 = p0 + TC_WARPS;
+      if (s_done[p0] && s_done[p1]) continue;
+      int px0, py0, px1, py1;
+      pixel_xy(tile, half, p0, A.ntx, px0, py0);
+      pixel_xy(tile, half, p1, A.ntx, px1, py1);
+      PixState st0{s_T[p0], s_cnt[p0], s_last[p0], s_done[p0] != 0};
+      PixState st1{s_T[p1], s_cnt[p1], s_last[p1], s_done[p1] != 0};
+      for (int k0 = 0; k0 < nsup && !(st0.done && st1.done); k0 += TC_K) {
+        const int nv = min(TC_K, nsup - k0);
+        bool inc0, inc1;
+        chunk_weight(s_rec + 2 * k0, nv, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR, half_w,
+                     teps, cb - start + k0, st0, inc0);
+        chunk_weight(s_rec + 2 * k0, nv, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR, half_w,
+                     teps, cb - start + k0, st1, inc1);
+        if (inc0 || inc1) s_live[k0 + lane] = 1;
       }
       if (lane == 0) {
-        s_T[p] = st.T;
-        s_cnt[p] = st.cnt;
-        s_last[p] = st.last;
-        s_done[p] = st.done;
+        s_T[p0] = st0.T;
+        s_cnt[p0] = st0.cnt;
+        s_last[p0] = st0.last;
+        s_done[p0] = st0.done;
+        s_T[p1] = st1.T;
+        s_cnt[p1] = st1.cnt;
+        s_last[p1] = st1.last;
+        s_done[p1] = st1.done;
       }
     }
     __syncthreads();
@@ -266,6 +277,49 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
                          ((uint32_t)(TC_P >> 4) << 24);
 
+  // ---- software pipeline: s_cidx (live-masked list indices) is resolved two
+  // chunks ahead, the coef values of the next chunk are held in registers
+  // while the current chunk's weights are computed.
+  constexpr int NQ = (NP * TC_K + 511) / 512;  // coef values per thread
+  __shared__ int s_cidx[3][TC_K];
+  const int nch_total = (end - start + TC_K - 1) / TC_K;
+  auto resolve = [&](int c) {  // threads < 32: entry -> idx if live else -1
+    if (tid < TC_K) {
+      int v = -1;
+      const int j = start + c * TC_K + tid;
+      if (c < nch_total && j < end) {
+        const int idx = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)j + 1].z));
+        v = A.live[idx] ? idx : -1;
+      }
+      s_cidx[c % 3][tid] = v;
+    }
+  };
+  float pre[NQ];
+  float4 prec[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  auto prefetch = [&](int c) {  // coef values + records of chunk c
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int q = tid + 512 * u;
+      float v = 0.f;
+      if (q < NP * TC_K && c < nch_total) {
+        const int k = q / NP, n = q - k * NP;
+        const int idx = s_cidx[c % 3][k];
+        const int64_t cc = col0 + n;
+        if (idx >= 0 && cc < A.Cp) v = __ldg(A.coef + (int64_t)idx * A.Cp + cc);
+      }
+      pre[u] = v;
+    }
+    if (tid < 2 * TC_K && c < nch_total) {
+      const int j0 = start + c * TC_K;
+      prec[0] = (j0 + (tid >> 1) < end) ? __ldg(A.pair_rec + 2 * (size_t)j0 + tid)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  resolve(0);
+  resolve(1);
+  __syncthreads();
+  prefetch(0);
+
   int nchunks = 0;
   for (int cb = start; cb < end; cb += TC_K, ++nchunks) {
     const int c = nchunks, stg = c & 1;
@@ -276,47 +330,49 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
     unsigned char* Bhi = base + 2 * A_BYTES;
     unsigned char* Blo = base + 2 * A_BYTES + B_BYTES;
     if (c >= 2) mbar_wait(smem_u32(&s_bar[stg]), ((c - 2) >> 1) & 1);
-    // records of this chunk
-    if (tid < 2 * TC_K) {
-      s_rec[stg][tid] = (tid < 2 * nk) ? __ldg(A.pair_rec + 2 * (size_t)cb + tid)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    // coef^T (B operand) rows n = channel, k = entry, zero for dead rows
-    for (int q = tid; q < NP * TC_K; q += blockDim.x) {
-      const int k = q / NP, n = q - k * NP;
-      float v = 0.f;
-      const int64_t cc = col0 + n;
-      if (k < nk && cc < A.Cp) {
-        const int idx = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)(cb + k) + 1].z));
-        if (A.live[idx]) v = __ldg(A.coef + (int64_t)idx * A.Cp + cc);
+    // commit the prefetched coef^T (B operand) and records of chunk c
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int q = tid + 512 * u;
+      if (q < NP * TC_K) {
+        const int k = q / NP, n = q - k * NP;
+        const float v = pre[u];
+        const float hi = tf32_hi(v);
+        const uint32_t off = sw128_off(n, k);
+        *(float*)(Bhi + off) = hi;
+        *(float*)(Blo + off) = v - hi;
       }
-      const float hi = tf32_hi(v);
-      const uint32_t off = sw128_off(n, k);
-      *(float*)(Bhi + off) = hi;
-      *(float*)(Blo + off) = v - hi;
     }
+    if (tid < 2 * TC_K) s_rec[stg][tid] = prec[0];
     __syncthreads();
-    // weights (A operand): warp w -> pixels w + 16 s
+    // launch the loads for chunk c+1 and resolve chunk c+2
+    prefetch(c + 1);
+    resolve(c + 2);
+    // weights (A operand): warp w -> pixels w + 16 s, two at a time
 #pragma unroll 1
-    for (int s = 0; s < TC_P / TC_WARPS; ++s) {
-      const int p = warp + TC_WARPS * s;
-      float wgt = 0.f;
-      if (!s_done[p]) {
-        int px, py;
-        pixel_xy(tile, half, p, A.ntx, px, py);
-        PixState st{s_T[p], 0, 0, false};
-        bool inc;
-        wgt = chunk_weight(s_rec[stg], nk, lane, (float)px + 0.5f, (float)py + 0.5f, wR, half_w,
-                           teps, 0, st, inc);
-        if (lane == 0) {
-          s_T[p] = st.T;
-          s_done[p] = st.done;
-        }
+    for (int s = 0; s < TC_P / TC_WARPS; s += 2) {
+      const int p0 = warp + TC_WARPS * s, p1 = p0 + TC_WARPS;
+      int px0, py0, px1, py1;
+      pixel_xy(tile, half, p0, A.ntx, px0, py0);
+      pixel_xy(tile, half, p1, A.ntx, px1, py1);
+      PixState st0{s_T[p0], 0, 0, s_done[p0] != 0};
+      PixState st1{s_T[p1], 0, 0, s_done[p1] != 0};
+      bool inc0, inc1;
+      const float w0 = chunk_weight(s_rec[stg], nk, lane, (float)px0 + 0.5f, (float)py0 + 0.5f,
+                                    wR, half_w, teps, 0, st0, inc0);
+      const float w1 = chunk_weight(s_rec[stg], nk, lane, (float)px1 + 0.5f, (float)py1 + 0.5f,
+                                    wR, half_w, teps, 0, st1, inc1);
+      if (lane == 0) {
+        s_T[p0] = st0.T;
+        s_done[p0] = st0.done;
+        s_T[p1] = st1.T;
+        s_done[p1] = st1.done;
       }
-      const float hi = tf32_hi(wgt);
-      const uint32_t off = sw128_off(p, lane);
-      *(float*)(Ahi + off) = hi;
-      *(float*)(Alo + off) = wgt - hi;
+      const float h0 = tf32_hi(w0), h1 = tf32_hi(w1);
+      *(float*)(Ahi + sw128_off(p0, lane)) = h0;
+      *(float*)(Alo + sw128_off(p0, lane)) = w0 - h0;
+      *(float*)(Ahi + sw128_off(p1, lane)) = h1;
+      *(float*)(Alo + sw128_off(p1, lane)) = w1 - h1;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::);
     __syncthreads();
