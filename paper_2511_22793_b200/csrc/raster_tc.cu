@@ -91,6 +91,92 @@ __device__ __forceinline__ float chunk_weight(const float4* s_rec, int nvalid, i
   return inc ? mul(Tb, a) : 0.f;
 }
 
+// Same chunk, four pixels per warp: the 8 lanes of group g = lane >> 3 own
+// one pixel, lane j = lane & 7 owns entries 4j .. 4j+3 (sequential product
+// inside the lane, 8-lane scan across lanes).  About half the instructions
+// per (pixel, entry) of the one-pixel-per-warp form.
+// Records of a chunk in shared memory as structure-of-arrays: field f of
+// entry e at soa[f * stride + e]; lane j reads its four entries of a field
+// with one conflict-free 16-byte load.
+__device__ __forceinline__ void chunk_weight4(const float* soa, int stride, int nvalid, int lane,
+                                              float pcx, float pcy, float wR, float half_w,
+                                              float teps, int list_pos0, PixState& st,
+                                              float (&w)[4], unsigned& incbits) {
+  const int j = lane & 7;
+  const bool live_px = !st.done;
+  float a[4], om[4];
+  bool v[4];
+  const float4 fmx = *(const float4*)(soa + 0 * stride + 4 * j);
+  const float4 fmy = *(const float4*)(soa + 1 * stride + 4 * j);
+  const float4 fca = *(const float4*)(soa + 2 * stride + 4 * j);
+  const float4 fcb = *(const float4*)(soa + 3 * stride + 4 * j);
+  const float4 fcc = *(const float4*)(soa + 4 * stride + 4 * j);
+  const float4 fop = *(const float4*)(soa + 5 * stride + 4 * j);
+  const float mx[4] = {fmx.x, fmx.y, fmx.z, fmx.w}, my[4] = {fmy.x, fmy.y, fmy.z, fmy.w};
+  const float ca[4] = {fca.x, fca.y, fca.z, fca.w}, cb[4] = {fcb.x, fcb.y, fcb.z, fcb.w};
+  const float cc[4] = {fcc.x, fcc.y, fcc.z, fcc.w}, op[4] = {fop.x, fop.y, fop.z, fop.w};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = 4 * j + u;
+    v[u] = live_px && e < nvalid;
+    a[u] = 0.f;
+    if (v[u]) {
+      a[u] = pixel_alpha<float>(pcx, pcy, mx[u], my[u], ca[u], cb[u], cc[u], op[u], wR, half_w)
+                 .alpha;
+    }
+    om[u] = sub(1.f, a[u]);
+  }
+  const float L = mul(mul(mul(om[0], om[1]), om[2]), om[3]);
+  float P = L;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const float t = __shfl_up_sync(0xffffffffu, P, d, 8);
+    if (j >= d) P = mul(t, P);
+  }
+  float Pex = __shfl_up_sync(0xffffffffu, P, 1, 8);
+  if (j == 0) Pex = 1.f;
+  float Tb[4];
+  Tb[0] = mul(st.T, Pex);
+  Tb[1] = mul(Tb[0], om[0]);
+  Tb[2] = mul(Tb[1], om[1]);
+  Tb[3] = mul(Tb[2], om[2]);
+  int first = 32;
+#pragma unroll
+  for (int u = 3; u >= 0; --u)
+    if (v[u] && Tb[u] < teps) first = 4 * j + u;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, d, 8));
+  int c = 0, m = -1;
+  unsigned bits = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const bool inc = v[u] && (4 * j + u) < first && a[u] > 0.f;
+    w[u] = inc ? mul(Tb[u], a[u]) : 0.f;
+    c += inc;
+    m = inc ? 4 * j + u : m;
+    bits |= (unsigned)inc << u;
+  }
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, d, 8);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, d, 8));
+  }
+  if (c) {
+    st.cnt += c;
+    st.last = list_pos0 + m + 1;
+  }
+  // transmittance handed to the next chunk
+  const int fu = first & 3;
+  const float Tsel = fu == 0 ? Tb[0] : fu == 1 ? Tb[1] : fu == 2 ? Tb[2] : Tb[3];
+  const float Tfirst = __shfl_sync(0xffffffffu, Tsel, (first >> 2) & 7, 8);
+  const float Tall = __shfl_sync(0xffffffffu, mul(st.T, P), 7, 8);
+  if (live_px) {
+    st.T = first < 32 ? Tfirst : Tall;
+    st.done = first < 32;
+  }
+  incbits = bits;
+}
+
 __device__ __forceinline__ void pixel_xy(int tile, int half, int p, int ntx, int& px, int& py) {
   const int tx_ = tile % ntx, ty = tile / ntx;
   px = tx_ * TILE + (p & 15);
@@ -101,7 +187,8 @@ __device__ __forceinline__ void pixel_xy(int tile, int half, int p, int ntx, int
 // 128 entries staged per barrier; 16 warps x 8 pixels each.
 __global__ void __launch_bounds__(512) k_raster_a(TcArgs A) {
   constexpr int SUP = 4 * TC_K;
-  __shared__ float4 s_rec[2 * SUP];
+  __shared__ __align__(16) float s_soa[6 * SUP];
+  __shared__ int s_sidx[SUP];
   __shared__ int s_live[SUP];
   __shared__ float s_T[TC_P];
   __shared__ int s_cnt[TC_P], s_last[TC_P], s_done[TC_P];
@@ -123,28 +210,49 @@ __global__ void __launch_bounds__(512) k_raster_a(TcArgs A) {
   for (int cb = start; cb < end; cb += SUP) {
     const int nsup = min(SUP, end - cb);
     __syncthreads();
-    if (tid < 2 * nsup) s_rec[tid] = __ldg(A.pair_rec + 2 * (size_t)cb + tid);
-    if (tid < SUP) s_live[tid] = 0;
+    if (tid < SUP) {
+      float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+      if (tid < nsup) {
+        r0 = __ldg(A.pair_rec + 2 * (size_t)(cb + tid));
+        r1 = __ldg(A.pair_rec + 2 * (size_t)(cb + tid) + 1);
+      }
+      s_soa[0 * SUP + tid] = r0.x;
+      s_soa[1 * SUP + tid] = r0.y;
+      s_soa[2 * SUP + tid] = r0.z;
+      s_soa[3 * SUP + tid] = r0.w;
+      s_soa[4 * SUP + tid] = r1.x;
+      s_soa[5 * SUP + tid] = r1.y;
+      s_sidx[tid] = __float_as_int(r1.z);
+      s_live[tid] = 0;
+    }
     __syncthreads();
-#pragma unroll 1
-    for (int s = 0; s < TC_P / TC_WARPS; s += 2) {
-      const int p0 = warp + TC_WARPS * s, p1 = p0 + TC_WARPS;
-      if (s_done[p0] && s_done[p1]) continue;
+    {
+      // lane group g = lane >> 3 owns pixel warp + 16 g (set 0) and
+      // warp + 16 (g + 4) (set 1); both sets advance together (ILP)
+      const int g = lane >> 3;
+      const int p0 = warp + TC_WARPS * g, p1 = warp + TC_WARPS * (g + 4);
       int px0, py0, px1, py1;
       pixel_xy(tile, half, p0, A.ntx, px0, py0);
       pixel_xy(tile, half, p1, A.ntx, px1, py1);
       PixState st0{s_T[p0], s_cnt[p0], s_last[p0], s_done[p0] != 0};
       PixState st1{s_T[p1], s_cnt[p1], s_last[p1], s_done[p1] != 0};
-      for (int k0 = 0; k0 < nsup && !(st0.done && st1.done); k0 += TC_K) {
+      for (int k0 = 0; k0 < nsup; k0 += TC_K) {
+        if (__all_sync(0xffffffffu, st0.done && st1.done)) break;
         const int nv = min(TC_K, nsup - k0);
-        bool inc0, inc1;
-        chunk_weight(s_rec + 2 * k0, nv, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR, half_w,
-                     teps, cb - start + k0, st0, inc0);
-        chunk_weight(s_rec + 2 * k0, nv, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR, half_w,
-                     teps, cb - start + k0, st1, inc1);
-        if (inc0 || inc1) s_live[k0 + lane] = 1;
+        float w0[4], w1[4];
+        unsigned b0, b1;
+        chunk_weight4(s_soa + k0, SUP, nv, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR,
+                      half_w, teps, cb - start + k0, st0, w0, b0);
+        chunk_weight4(s_soa + k0, SUP, nv, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR,
+                      half_w, teps, cb - start + k0, st1, w1, b1);
+        const unsigned b = b0 | b1;
+        if (b) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if ((b >> u) & 1u) s_live[k0 + 4 * (lane & 7) + u] = 1;
+        }
       }
-      if (lane == 0) {
+      if ((lane & 7) == 0) {
         s_T[p0] = st0.T;
         s_cnt[p0] = st0.cnt;
         s_last[p0] = st0.last;
@@ -157,7 +265,7 @@ __global__ void __launch_bounds__(512) k_raster_a(TcArgs A) {
     }
     __syncthreads();
     if (tid < nsup && s_live[tid]) {
-      const int idx = __float_as_int(s_rec[2 * tid + 1].z);
+      const int idx = s_sidx[tid];
       if (A.live[idx] == 0 && atomicExch((int*)A.live + idx, 1) == 0) {
         const int pos = atomicAdd(A.counters + GSPARC_CNT_LIVE, 1);
         A.live_list[pos] = idx;
@@ -235,7 +343,7 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
   constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  __shared__ float4 s_rec[2][2 * TC_K];
+  __shared__ __align__(16) float s_soa[2][6 * TC_K];
   __shared__ float s_T[TC_P];
   __shared__ int s_done[TC_P];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -309,10 +417,11 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
       }
       pre[u] = v;
     }
-    if (tid < 2 * TC_K && c < nch_total) {
-      const int j0 = start + c * TC_K;
-      prec[0] = (j0 + (tid >> 1) < end) ? __ldg(A.pair_rec + 2 * (size_t)j0 + tid)
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < TC_K && c < nch_total) {
+      const int j = start + c * TC_K + tid;
+      const bool ok = j < end;
+      prec[0] = ok ? __ldg(A.pair_rec + 2 * (size_t)j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      prec[1] = ok ? __ldg(A.pair_rec + 2 * (size_t)j + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   resolve(0);
@@ -343,36 +452,52 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
         *(float*)(Blo + off) = v - hi;
       }
     }
-    if (tid < 2 * TC_K) s_rec[stg][tid] = prec[0];
+    if (tid < TC_K) {
+      float* so = s_soa[stg];
+      so[0 * TC_K + tid] = prec[0].x;
+      so[1 * TC_K + tid] = prec[0].y;
+      so[2 * TC_K + tid] = prec[0].z;
+      so[3 * TC_K + tid] = prec[0].w;
+      so[4 * TC_K + tid] = prec[1].x;
+      so[5 * TC_K + tid] = prec[1].y;
+    }
     __syncthreads();
     // launch the loads for chunk c+1 and resolve chunk c+2
     prefetch(c + 1);
     resolve(c + 2);
-    // weights (A operand): warp w -> pixels w + 16 s, two at a time
-#pragma unroll 1
-    for (int s = 0; s < TC_P / TC_WARPS; s += 2) {
-      const int p0 = warp + TC_WARPS * s, p1 = p0 + TC_WARPS;
+    // weights (A operand): lane group g owns pixels warp + 16 g and
+    // warp + 16 (g + 4); lane j writes entries 4j..4j+3 = one 16-byte chunk
+    {
+      const int g = lane >> 3, j = lane & 7;
+      const int p0 = warp + TC_WARPS * g, p1 = warp + TC_WARPS * (g + 4);
       int px0, py0, px1, py1;
       pixel_xy(tile, half, p0, A.ntx, px0, py0);
       pixel_xy(tile, half, p1, A.ntx, px1, py1);
       PixState st0{s_T[p0], 0, 0, s_done[p0] != 0};
       PixState st1{s_T[p1], 0, 0, s_done[p1] != 0};
-      bool inc0, inc1;
-      const float w0 = chunk_weight(s_rec[stg], nk, lane, (float)px0 + 0.5f, (float)py0 + 0.5f,
-                                    wR, half_w, teps, 0, st0, inc0);
-      const float w1 = chunk_weight(s_rec[stg], nk, lane, (float)px1 + 0.5f, (float)py1 + 0.5f,
-                                    wR, half_w, teps, 0, st1, inc1);
-      if (lane == 0) {
+      float w0[4], w1[4];
+      unsigned b0, b1;
+      chunk_weight4(s_soa[stg], TC_K, nk, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR, half_w,
+                    teps, 0, st0, w0, b0);
+      chunk_weight4(s_soa[stg], TC_K, nk, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR, half_w,
+                    teps, 0, st1, w1, b1);
+      if (j == 0) {
         s_T[p0] = st0.T;
         s_done[p0] = st0.done;
         s_T[p1] = st1.T;
         s_done[p1] = st1.done;
       }
-      const float h0 = tf32_hi(w0), h1 = tf32_hi(w1);
-      *(float*)(Ahi + sw128_off(p0, lane)) = h0;
-      *(float*)(Alo + sw128_off(p0, lane)) = w0 - h0;
-      *(float*)(Ahi + sw128_off(p1, lane)) = h1;
-      *(float*)(Alo + sw128_off(p1, lane)) = w1 - h1;
+      float4 h, l;
+      h = make_float4(tf32_hi(w0[0]), tf32_hi(w0[1]), tf32_hi(w0[2]), tf32_hi(w0[3]));
+      l = make_float4(w0[0] - h.x, w0[1] - h.y, w0[2] - h.z, w0[3] - h.w);
+      const uint32_t o0 = (uint32_t)(p0 * 128 + ((j ^ (p0 & 7)) << 4));
+      *(float4*)(Ahi + o0) = h;
+      *(float4*)(Alo + o0) = l;
+      h = make_float4(tf32_hi(w1[0]), tf32_hi(w1[1]), tf32_hi(w1[2]), tf32_hi(w1[3]));
+      l = make_float4(w1[0] - h.x, w1[1] - h.y, w1[2] - h.z, w1[3] - h.w);
+      const uint32_t o1 = (uint32_t)(p1 * 128 + ((j ^ (p1 & 7)) << 4));
+      *(float4*)(Ahi + o1) = h;
+      *(float4*)(Alo + o1) = l;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::);
     __syncthreads();
