@@ -333,20 +333,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity));
 }
 
-// NP: channel columns per CTA (multiple of 8, <= 256); chunk of the
-// channel axis is blockIdx.y.
+// NP: channel columns per CTA (multiple of 8, <= 256); the channel axis is
+// split over blockIdx.y.  Single operand stage: the weights of chunk c and
+// the coef values of chunk c are computed / loaded into registers while the
+// MMAs of chunk c-1 run, then stored once those MMAs have retired, so a CTA
+// needs ~60 KB of shared memory and three CTAs share an SM.
 template <int NP>
-__global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
+__global__ void __launch_bounds__(512, 2) k_raster_b(TcArgs A) {
   constexpr int A_BYTES = TC_P * 128;  // 16 KB per operand copy
   constexpr int B_BYTES = NP * 128;
-  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;  // hi + lo of A and B
   constexpr uint32_t TMEM_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  constexpr int NQ = (NP * TC_K + 511) / 512;  // coef values per thread
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(16) float s_soa[2][6 * TC_K];
+  unsigned char* Ahi = sm;
+  unsigned char* Alo = sm + A_BYTES;
+  unsigned char* Bhi = sm + 2 * A_BYTES;
+  unsigned char* Blo = sm + 2 * A_BYTES + B_BYTES;
+  __shared__ __align__(16) float s_soa[6 * TC_K];
+  __shared__ int s_cidx[3][TC_K];
   __shared__ float s_T[TC_P];
   __shared__ int s_done[TC_P];
-  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint32_t s_tmem;
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
@@ -358,6 +366,7 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) vis = max(vis, A.wstop[tile * 8 + half * 4 + q]);
   const int end = start + vis;
+  const int nch_total = (vis + TC_K - 1) / TC_K;
   const float wR = (float)A.w, half_w = (float)(A.w / 2.0), teps = A.t_eps;
 
   if (tid < TC_P) {
@@ -367,8 +376,7 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
     s_done[tid] = !(px < A.w && py < A.h);
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::);
   }
   if (warp == 0) {
@@ -377,34 +385,21 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::);
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::);
-  const uint32_t tmem = s_tmem;
-  // instruction descriptor: D f32, A/B tf32, K-major both, N = NP, M = 128
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
-                         ((uint32_t)(TC_P >> 4) << 24);
-
-  // ---- software pipeline: s_cidx (live-masked list indices) is resolved two
-  // chunks ahead, the coef values of the next chunk are held in registers
-  // while the current chunk's weights are computed.
-  constexpr int NQ = (NP * TC_K + 511) / 512;  // coef values per thread
-  __shared__ int s_cidx[3][TC_K];
-  const int nch_total = (end - start + TC_K - 1) / TC_K;
-  auto resolve = [&](int c) {  // threads < 32: entry -> idx if live else -1
+  // live-masked list indices, resolved two chunks ahead (threads < 32)
+  auto resolve = [&](int c) {
     if (tid < TC_K) {
       int v = -1;
-      const int j = start + c * TC_K + tid;
-      if (c < nch_total && j < end) {
-        const int idx = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)j + 1].z));
+      const int jj = start + c * TC_K + tid;
+      if (c < nch_total && jj < end) {
+        const int idx = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)jj + 1].z));
         v = A.live[idx] ? idx : -1;
       }
       s_cidx[c % 3][tid] = v;
     }
   };
   float pre[NQ];
-  float4 prec[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-  auto prefetch = [&](int c) {  // coef values + records of chunk c
+  float4 prec0 = make_float4(0.f, 0.f, 0.f, 0.f), prec1 = prec0;
+  auto prefetch = [&](int c) {  // coef values + records of chunk c -> registers
 #pragma unroll
     for (int u = 0; u < NQ; ++u) {
       const int q = tid + 512 * u;
@@ -418,28 +413,54 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
       pre[u] = v;
     }
     if (tid < TC_K && c < nch_total) {
-      const int j = start + c * TC_K + tid;
-      const bool ok = j < end;
-      prec[0] = ok ? __ldg(A.pair_rec + 2 * (size_t)j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      prec[1] = ok ? __ldg(A.pair_rec + 2 * (size_t)j + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int jj = start + c * TC_K + tid;
+      const bool ok = jj < end;
+      prec0 = ok ? __ldg(A.pair_rec + 2 * (size_t)jj) : make_float4(0.f, 0.f, 0.f, 0.f);
+      prec1 = ok ? __ldg(A.pair_rec + 2 * (size_t)jj + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   resolve(0);
   resolve(1);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::);
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::);
+  const uint32_t tmem = s_tmem;
+  // instruction descriptor: D f32, A/B tf32, K-major both, N = NP, M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
+                         ((uint32_t)(TC_P >> 4) << 24);
   prefetch(0);
 
+  const int g = lane >> 3, j = lane & 7;
+  const int p0 = warp + TC_WARPS * g, p1 = warp + TC_WARPS * (g + 4);
+  int px0, py0, px1, py1;
+  pixel_xy(tile, half, p0, A.ntx, px0, py0);
+  pixel_xy(tile, half, p1, A.ntx, px1, py1);
+  PixState st0{1.f, 0, 0, s_done[p0] != 0};
+  PixState st1{1.f, 0, 0, s_done[p1] != 0};
+
   int nchunks = 0;
-  for (int cb = start; cb < end; cb += TC_K, ++nchunks) {
-    const int c = nchunks, stg = c & 1;
-    const int nk = min(TC_K, end - cb);
-    unsigned char* base = sm + stg * STAGE;
-    unsigned char* Ahi = base;
-    unsigned char* Alo = base + A_BYTES;
-    unsigned char* Bhi = base + 2 * A_BYTES;
-    unsigned char* Blo = base + 2 * A_BYTES + B_BYTES;
-    if (c >= 2) mbar_wait(smem_u32(&s_bar[stg]), ((c - 2) >> 1) & 1);
-    // commit the prefetched coef^T (B operand) and records of chunk c
+  for (int c = 0; c < nch_total; ++c) {
+    const int nk = min(TC_K, end - (start + c * TC_K));
+    // records of chunk c (the previous chunk's readers passed barrier 2)
+    if (tid < TC_K) {
+      s_soa[0 * TC_K + tid] = prec0.x;
+      s_soa[1 * TC_K + tid] = prec0.y;
+      s_soa[2 * TC_K + tid] = prec0.z;
+      s_soa[3 * TC_K + tid] = prec0.w;
+      s_soa[4 * TC_K + tid] = prec1.x;
+      s_soa[5 * TC_K + tid] = prec1.y;
+    }
+    __syncthreads();
+    // weights of chunk c in registers
+    float w0[4], w1[4];
+    unsigned b0, b1;
+    chunk_weight4(s_soa, TC_K, nk, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR, half_w, teps,
+                  0, st0, w0, b0);
+    chunk_weight4(s_soa, TC_K, nk, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR, half_w, teps,
+                  0, st1, w1, b1);
+    const bool all_done = (j == 0) && st0.done && st1.done;
+    // operands of chunk c-1 are free once its MMAs retired
+    if (c >= 1) mbar_wait(smem_u32(&s_bar), (c - 1) & 1);
 #pragma unroll
     for (int u = 0; u < NQ; ++u) {
       const int q = tid + 512 * u;
@@ -452,44 +473,9 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
         *(float*)(Blo + off) = v - hi;
       }
     }
-    if (tid < TC_K) {
-      float* so = s_soa[stg];
-      so[0 * TC_K + tid] = prec[0].x;
-      so[1 * TC_K + tid] = prec[0].y;
-      so[2 * TC_K + tid] = prec[0].z;
-      so[3 * TC_K + tid] = prec[0].w;
-      so[4 * TC_K + tid] = prec[1].x;
-      so[5 * TC_K + tid] = prec[1].y;
-    }
-    __syncthreads();
-    // launch the loads for chunk c+1 and resolve chunk c+2
-    prefetch(c + 1);
-    resolve(c + 2);
-    // weights (A operand): lane group g owns pixels warp + 16 g and
-    // warp + 16 (g + 4); lane j writes entries 4j..4j+3 = one 16-byte chunk
     {
-      const int g = lane >> 3, j = lane & 7;
-      const int p0 = warp + TC_WARPS * g, p1 = warp + TC_WARPS * (g + 4);
-      int px0, py0, px1, py1;
-      pixel_xy(tile, half, p0, A.ntx, px0, py0);
-      pixel_xy(tile, half, p1, A.ntx, px1, py1);
-      PixState st0{s_T[p0], 0, 0, s_done[p0] != 0};
-      PixState st1{s_T[p1], 0, 0, s_done[p1] != 0};
-      float w0[4], w1[4];
-      unsigned b0, b1;
-      chunk_weight4(s_soa[stg], TC_K, nk, lane, (float)px0 + 0.5f, (float)py0 + 0.5f, wR, half_w,
-                    teps, 0, st0, w0, b0);
-      chunk_weight4(s_soa[stg], TC_K, nk, lane, (float)px1 + 0.5f, (float)py1 + 0.5f, wR, half_w,
-                    teps, 0, st1, w1, b1);
-      if (j == 0) {
-        s_T[p0] = st0.T;
-        s_done[p0] = st0.done;
-        s_T[p1] = st1.T;
-        s_done[p1] = st1.done;
-      }
-      float4 h, l;
-      h = make_float4(tf32_hi(w0[0]), tf32_hi(w0[1]), tf32_hi(w0[2]), tf32_hi(w0[3]));
-      l = make_float4(w0[0] - h.x, w0[1] - h.y, w0[2] - h.z, w0[3] - h.w);
+      float4 h = make_float4(tf32_hi(w0[0]), tf32_hi(w0[1]), tf32_hi(w0[2]), tf32_hi(w0[3]));
+      float4 l = make_float4(w0[0] - h.x, w0[1] - h.y, w0[2] - h.z, w0[3] - h.w);
       const uint32_t o0 = (uint32_t)(p0 * 128 + ((j ^ (p0 & 7)) << 4));
       *(float4*)(Ahi + o0) = h;
       *(float4*)(Alo + o0) = l;
@@ -499,8 +485,11 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
       *(float4*)(Ahi + o1) = h;
       *(float4*)(Alo + o1) = l;
     }
+    // next chunk's loads fly while this chunk's MMAs run
+    prefetch(c + 1);
+    resolve(c + 2);
     asm volatile("fence.proxy.async.shared::cta;" ::);
-    __syncthreads();
+    const int ndone = __syncthreads_count(all_done);
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::);
       const uint32_t a_hi = smem_u32(Ahi), a_lo = smem_u32(Alo);
@@ -514,16 +503,12 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
         mma_tf32(tmem, umma_desc_sw128(a_lo + koff), umma_desc_sw128(b_hi + koff), idesc, 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
-                       "r"(smem_u32(&s_bar[stg])));
+                       "r"(smem_u32(&s_bar)));
     }
-    if (__syncthreads_count(tid < TC_P ? s_done[tid] : 1) == (int)blockDim.x) {
-      ++nchunks;
-      break;
-    }
+    nchunks = c + 1;
+    if (ndone == TC_P / 2) break;  // 16 warps x 4 groups x 2 pixels
   }
-  // drain the MMA pipeline
-  if (nchunks >= 1) mbar_wait(smem_u32(&s_bar[(nchunks - 1) & 1]), ((nchunks - 1) >> 1) & 1);
-  if (nchunks >= 2) mbar_wait(smem_u32(&s_bar[(nchunks - 2) & 1]), ((nchunks - 2) >> 1) & 1);
+  if (nchunks >= 1) mbar_wait(smem_u32(&s_bar), (nchunks - 1) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::);
   // epilogue: warps 0..3 read TMEM lanes 32w..32w+31 (= pixels)
   if (warp < 4) {
@@ -544,15 +529,15 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::);
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0u;
+        for (int q = 0; q < 8; ++q) v[q] = 0u;
       }
       if (inside) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int64_t cc = col0 + c0 + j;
+        for (int q = 0; q < 8; ++q) {
+          const int64_t cc = col0 + c0 + q;
           if (cc < A.Cp) {
             const int64_t b = cc / A.C, ch = cc - b * A.C;
-            A.img[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch] = __uint_as_float(v[j]);
+            A.img[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch] = __uint_as_float(v[q]);
           }
         }
       }
@@ -569,7 +554,7 @@ __global__ void __launch_bounds__(512, 1) k_raster_b(TcArgs A) {
 template <int NP>
 static void launch_b(const TcArgs& A, int chunks, cudaStream_t st) {
   constexpr int STAGE = 2 * TC_P * 128 + 2 * NP * 128;
-  const size_t smem = 2 * STAGE + 1024;
+  const size_t smem = STAGE + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_raster_b<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
