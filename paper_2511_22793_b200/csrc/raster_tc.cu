@@ -385,17 +385,17 @@ __global__ void __launch_bounds__(512, 2) k_raster_b(TcArgs A) {
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
-  // live-masked list indices, resolved two chunks ahead (threads < 32)
-  auto resolve = [&](int c) {
+  // list indices of chunk c (threads < 32).  No live mask is needed: coef
+  // rows of Gaussians that are not live were either zero-initialised with
+  // the frame or written by an earlier render, so they are finite and meet a
+  // weight of exactly zero.
+  auto idx_of = [&](int c) -> int {
+    int v = -1;
     if (tid < TC_K) {
-      int v = -1;
       const int jj = start + c * TC_K + tid;
-      if (c < nch_total && jj < end) {
-        const int idx = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)jj + 1].z));
-        v = A.live[idx] ? idx : -1;
-      }
-      s_cidx[c % 3][tid] = v;
+      if (c < nch_total && jj < end) v = __float_as_int(__ldg(&A.pair_rec[2 * (size_t)jj + 1].z));
     }
+    return v;
   };
   float pre[NQ];
   float4 prec0 = make_float4(0.f, 0.f, 0.f, 0.f), prec1 = prec0;
@@ -419,8 +419,11 @@ __global__ void __launch_bounds__(512, 2) k_raster_b(TcArgs A) {
       prec1 = ok ? __ldg(A.pair_rec + 2 * (size_t)jj + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
-  resolve(0);
-  resolve(1);
+  if (tid < TC_K) {
+    s_cidx[0][tid] = idx_of(0);
+    s_cidx[1][tid] = idx_of(1);
+  }
+  int ridx = idx_of(2);  // register-carried: stored one iteration later
   asm volatile("tcgen05.fence::before_thread_sync;" ::);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::);
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(512, 2) k_raster_b(TcArgs A) {
     const int nk = min(TC_K, end - (start + c * TC_K));
     // records of chunk c (the previous chunk's readers passed barrier 2)
     if (tid < TC_K) {
+      s_cidx[(c + 2) % 3][tid] = ridx;
       s_soa[0 * TC_K + tid] = prec0.x;
       s_soa[1 * TC_K + tid] = prec0.y;
       s_soa[2 * TC_K + tid] = prec0.z;
@@ -487,10 +491,10 @@ __global__ void __launch_bounds__(512, 2) k_raster_b(TcArgs A) {
     }
     // next chunk's loads fly while this chunk's MMAs run
     prefetch(c + 1);
-    resolve(c + 2);
+    ridx = idx_of(c + 3);
     asm volatile("fence.proxy.async.shared::cta;" ::);
     const int ndone = __syncthreads_count(all_done);
-    if (tid == 0) {
+    if (tid == 512 - 32) {  // the MMA issuer lives in the last warp
       asm volatile("tcgen05.fence::after_thread_sync;" ::);
       const uint32_t a_hi = smem_u32(Ahi), a_lo = smem_u32(Alo);
       const uint32_t b_hi = smem_u32(Bhi), b_lo = smem_u32(Blo);

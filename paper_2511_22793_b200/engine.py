@@ -46,7 +46,9 @@ class Frame:
                                       int(bool(with_backward)),
                                       ctypes.byref(L)))
         self.layout = L
-        self.buf = torch.empty(int(L.total_bytes), dtype=torch.uint8,
+        # zero-initialised once: coef rows of never-live Gaussians must be
+        # finite (the tensor-core accumulation multiplies them by 0)
+        self.buf = torch.zeros(int(L.total_bytes), dtype=torch.uint8,
                                device=device)
         self.n, self.w, self.h = int(n), int(w), int(h)
         self.channels = int(channels)
