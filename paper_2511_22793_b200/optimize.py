@@ -22,6 +22,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib
+from . import dp
 from .engine import LossWorkspace, Renderer, split_flat
 from .image import SpectrumImage
 from .rasterizer import ParamGradients, rasterize_forward
@@ -295,8 +296,7 @@ class Trainer:
 
     def _allreduce(self):
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+            dp.allreduce_sum(self.grad, self.group)
 
     def capture(self):
         """Capture gather+forward+loss+backward(+Adam when single-rank) into a
@@ -320,7 +320,7 @@ class Trainer:
         gi = np.asarray(global_indices, np.int64).reshape(-1)
         if gi.size != self.B:
             raise ValueError(f"expected {self.B} indices, got {gi.size}")
-        local = gi[self.rank * self.Bl:(self.rank + 1) * self.Bl]
+        local = dp.shard(gi, self.rank, self.world)
         self.idx.copy_(torch.as_tensor(local), non_blocking=True)
 
     def step(self, global_indices=None):
