@@ -38,6 +38,7 @@ CONFIGS = {
     # name: (N, W, H, F, tx per step)
     "c3": (50_000, 360, 90, 52, 1),
     "c1": (4_096, 360, 90, 1, 64),
+    "c2": (16_384, 360, 90, 1, 32),   # training step (fwd+loss+bwd+Adam)
 }
 
 
@@ -202,7 +203,9 @@ def run_reference(args):
 def workload_config(name):
     n, w, h, F, B = CONFIGS[name]
     desc = {"c3": "config 3: CSI multi-frequency per-TX render latency",
-            "c1": "config 1: batched forward of 64 TX positions"}[name]
+            "c1": "config 1: batched forward of 64 TX positions",
+            "c2": "config 2: training step (render + L1/SSIM + backward + "
+                  "Adam) on a batch of 32 TX"}[name]
     return {"workload": f"{desc}; {n} Gaussians, {h}x{w} hemisphere x {F} "
                         f"subcarrier(s) ({2 * F} channels), {B} TX per step",
             "n_gaussians": n, "height": h, "width": w, "subcarriers": F,
@@ -458,10 +461,79 @@ def roofline_entry(dom, stages, n, P, C, B, h, w, live, pairs, hbm):
                     "see profiles/ for issue-slot utilisation"}
 
 
+def run_train(args):
+    """--config c2: device train step (K2..K8), batch of 32 TX per step,
+    data-parallel over ranks (global batch split, NCCL all-reduce)."""
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_22793_b200 import ViewPose
+    from paper_2511_22793_b200.optimize import TrainConfig, Trainer
+    n, w, h, F, B = CONFIGS[args.config]
+    cloud = bench_cloud(n, F)
+    S = 5000                                  # config-4 sized sample table
+    txs = sample_tx(7, S)
+    gt = np.random.default_rng(7).random((S, h, w, 1), dtype=np.float32) * 0.5
+    cfg = TrainConfig(width=w, height=h, batch_tx=B)
+    tr = Trainer(cloud, ViewPose(np.zeros(3)), cfg, txs, gt)
+    if not args.no_graph:
+        tr.capture()
+    rng = np.random.Generator(np.random.PCG64(0))
+    batches = [rng.integers(S, size=B) for _ in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        tr.step(batches[i])
+    torch.cuda.synchronize()
+    ok = tr.check()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for i in range(args.steps):
+            stats = tr.step(batches[args.warmup + i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    loss = float(stats[:, 0].mean().item())
+    ok = tr.check() and ok
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    line = None
+    if rank == 0:
+        line = {"metric": "train iterations/s (global batch 32 TX)",
+                "value": 1e3 / ms, "unit": "it/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (bench scene, random magnitude targets)",
+                "config": dict(workload_config(args.config),
+                               parallelism=f"dp{world}"),
+                "clocks": clocks.summary(), "renders_per_s": B * 1e3 / ms,
+                "last_loss": loss, "healthy": bool(ok),
+                "gpu_launches": None}
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c2":
+        return run_train(args)
     return run_ours(args)
 
 
