@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GSPARC_ABI_VERSION 1
+#define GSPARC_ABI_VERSION 2
 
 enum {
   GSPARC_OK = 0,
@@ -117,10 +117,17 @@ typedef struct gsparc_frame_layout {
   int64_t off_coef;       /* f32/f64 [n,channels] s/d per Gaussian,TX   */
   int64_t off_gcoef;      /* f32/f64 [n,channels] dL/dcoef (backward)   */
   int64_t off_ggeo;       /* f32/f64 [n,8] dL/d(conic3,mean2d2,sigma)   */
-  int64_t off_pair_rec;   /* f32  [pair_capacity,8] raster record per list
-                             entry (f32 frames), list order               */
+  int64_t off_pair_rec;   /* unused since ABI 2 (0)                       */
   int64_t off_wstop;      /* i32  [ntiles*8] visited list prefix per
                              32-pixel warp (2 rows x 16 px)               */
+  int64_t off_rrec;       /* f32  [n,8] f32 raster record {mx,my,qa,qb,
+                             qc,opacity,xr,yr} (f32 frames)               */
+  int64_t off_ch_idx;     /* u32  [slots,32] per half-tile CTA: source
+                             indices of the culled list, 32 per chunk     */
+  int64_t off_ch_T;       /* f32  [slots,128] transmittance of the CTA's
+                             128 pixels at the start of every chunk       */
+  int64_t off_ch_n;       /* i32  [2*ntiles] chunks with a contribution   */
+  int64_t ch_slots;       /* chunk slots (>= 2*(pairs+31*ntiles)/32 + 2) */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

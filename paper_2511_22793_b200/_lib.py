@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsparc_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
 F32, F64 = 0, 1
@@ -40,7 +40,8 @@ class CView(ctypes.Structure):
 _LAYOUT_OFFSETS = ("key", "rec32", "rec64", "rect", "counters", "tile_count",
                    "tile_cursor", "tile_start", "tile_stop", "pairs", "T",
                    "count", "last", "live", "live_list", "coef", "gcoef",
-                   "ggeo", "pair_rec", "wstop")
+                   "ggeo", "pair_rec", "wstop", "rrec", "ch_idx", "ch_T",
+                   "ch_n")
 
 
 class CLayout(ctypes.Structure):
@@ -48,7 +49,8 @@ class CLayout(ctypes.Structure):
                  ("channels", c_i64)] +
                 [(k, c_i32) for k in ("width", "height", "ntx", "nty", "ntiles",
                                       "dtype", "with_backward", "reserved")] +
-                [("off_" + k, c_i64) for k in _LAYOUT_OFFSETS])
+                [("off_" + k, c_i64) for k in _LAYOUT_OFFSETS] +
+                [("ch_slots", c_i64)])
 
 
 class CAdamConfig(ctypes.Structure):

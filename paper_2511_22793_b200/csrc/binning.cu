@@ -446,7 +446,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   }
   int idx_bits = 8;
   while (idx_bits < 32 && ((int64_t)1 << idx_bits) < L.n) idx_bits += 8;
-  float4* pair_rec = L.dtype == GSPARC_F64 ? nullptr : (float4*)(frame + L.off_pair_rec);
+  float4* pair_rec = nullptr;  // the f32 raster gathers rrec by index
   k_tile_sort<<<L.ntiles, RS_T, smem_sort, st>>>(A.pairs, A.tile_start, A.key, A.counters,
                                            (const float4*)(frame + L.off_rec32), pair_rec,
                                            idx_bits);

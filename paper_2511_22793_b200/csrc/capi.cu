@@ -140,8 +140,16 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_coef = take(esz * nn * channels);
   L.off_gcoef = with_backward ? take(esz * nn * channels) : 0;
   L.off_ggeo = with_backward ? take(esz * nn * 8) : 0;
-  L.off_pair_rec = dtype == GSPARC_F32 ? take(32 * pair_capacity) : 0;
+  L.off_pair_rec = 0;
   L.off_wstop = take(sizeof(int) * L.ntiles * 8);
+  // f32 raster (raster_px.cu): records + per half-tile chunk lists and
+  // transmittance checkpoints.  A CTA's chunks never exceed ceil(len/32),
+  // so 2 * floor((tile_start + 31 t) / 32) is a valid per-tile slot base.
+  L.ch_slots = 2 * ((pair_capacity + 31 * (int64_t)L.ntiles) / 32) + 2 * L.ntiles + 2;
+  L.off_rrec = take(dtype == GSPARC_F32 ? 32 * nn : 0);
+  L.off_ch_idx = take(dtype == GSPARC_F32 ? 4 * 32 * L.ch_slots : 0);
+  L.off_ch_T = take(dtype == GSPARC_F32 ? 4 * 128 * L.ch_slots : 0);
+  L.off_ch_n = take(sizeof(int) * 2 * L.ntiles);
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

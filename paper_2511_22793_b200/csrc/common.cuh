@@ -143,6 +143,59 @@ __device__ __forceinline__ AlphaOut<R> pixel_alpha(R pcx, R pcy, R mx, R my, R c
   return o;
 }
 
+// ---- f32 raster alpha (K4 f32 passes and the f32 backward K5) ----------
+// Raster record rrec (written by K2, f32, source order), 2 x float4:
+//   {mx, my, qa, qb} {qc, opacity, xr, yr}
+// with the conic pre-scaled into the base-2 exponent,
+//   q' = -0.5 * log2(e) * q = dx (qa dx + qb dy) + qc dy^2,
+//   qa = -0.5 log2e ca,  qb = -log2e cb,  qc = -0.5 log2e cc   (f64 -> f32),
+// so alpha = min(op * 2^q', 0.99), zeroed below 1/255 (rasterizer.py:177-183),
+// costs 16 instructions.  The azimuth wrap is dx - w * rint(dx / w) on
+// dx = pcx - mx in (-w, w) (the numpy remainder of rasterizer.py:177 up to the
+// half-way tie).  Against numpy's operation order this moves alpha by a few
+// ulp, like the 2-ulp exp before it; tests count the resulting threshold
+// flips.  (xr, yr): conservative half extents of the alpha >= 1/255 ellipse,
+// sqrt(2 ln(255 op) Sigma_ii) (1 + 1e-4) + 0.01 px (-1 if 255 op <= 1); used
+// only to skip entries that are zero for every pixel of a CTA (exact: such
+// an entry multiplies T by 1 and is never included).
+constexpr double LOG2E = 1.4426950408889634;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+struct FastAlpha {
+  float alpha, raw, g, dx, dy;
+};
+
+__device__ __forceinline__ FastAlpha fast_alpha_full(float pcx, float pcy, float4 r0, float4 r1,
+                                                     float w, float inv_w) {
+  FastAlpha o;
+  const float dxr = pcx - r0.x;
+  o.dx = fmaf(-w, rintf(dxr * inv_w), dxr);
+  o.dy = pcy - r0.y;
+  const float t = fmaf(r0.w, o.dy, r0.z * o.dx);
+  const float qp = fmaf(o.dx, t, (r1.x * o.dy) * o.dy);
+  o.g = ex2_approx(qp);
+  o.raw = r1.y * o.g;
+  const float a = fminf(o.raw, ALPHA_MAX_F);
+  o.alpha = a < ALPHA_MIN_F ? 0.f : a;
+  return o;
+}
+
+__device__ __forceinline__ float fast_alpha(float pcx, float pcy, float4 r0, float4 r1, float w,
+                                            float inv_w) {
+  const float dxr = pcx - r0.x;
+  const float dx = fmaf(-w, rintf(dxr * inv_w), dxr);
+  const float dy = pcy - r0.y;
+  const float t = fmaf(r0.w, dy, r0.z * dx);
+  const float qp = fmaf(dx, t, (r1.x * dy) * dy);
+  const float a = fminf(r1.y * ex2_approx(qp), ALPHA_MAX_F);
+  return a < ALPHA_MIN_F ? 0.f : a;
+}
+
 template <typename R>
 struct Rec {  // raster record in the raster precision
   R mx, my, ca, cb, cc, op;

@@ -14,7 +14,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
                const gsparc_frame_layout& L, char* frame, cudaStream_t st);
 int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                           double t_eps, int pass, void* img, cudaStream_t st);
-int launch_raster_tc(const gsparc_frame_layout& L, char* frame, int n_tx, int C, double t_eps,
+int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C, double t_eps,
                      int pass, void* img, cudaStream_t st);
 int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                            const void* dL, cudaStream_t st);

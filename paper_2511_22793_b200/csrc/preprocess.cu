@@ -18,6 +18,7 @@ struct PrepArgs {
   uint64_t* key;
   float4* rec32;
   double* rec64;
+  float4* rrec;
   int4* rect;
   int* counters;
   int* tile_count;
@@ -201,6 +202,19 @@ __global__ void __launch_bounds__(128) k_preprocess(PrepArgs A) {
     A.key[i] = k;
     A.rec32[2 * i] = make_float4((float)mx, (float)my, (float)(c / det), (float)(-b / det));
     A.rec32[2 * i + 1] = make_float4((float)(a / det), (float)opac, (float)theta, (float)phi);
+    if (A.rrec) {  // f32 raster record (common.cuh "f32 raster alpha")
+      const double ca_ = c / det, cb_ = -b / det, cc_ = a / det;
+      float xr = -1.f, yr = -1.f;
+      const double o255 = 255.0 * opac;
+      if (o255 > 1.0) {
+        const double Q = 2.0 * log(o255);
+        xr = (float)(sqrt(Q * a) * (1.0 + 1e-4) + 0.01);
+        yr = (float)(sqrt(Q * fmax(c, 0.0)) * (1.0 + 1e-4) + 0.01);
+      }
+      A.rrec[2 * i] = make_float4((float)mx, (float)my, (float)(-0.5 * LOG2E * ca_),
+                                  (float)(-LOG2E * cb_));
+      A.rrec[2 * i + 1] = make_float4((float)(-0.5 * LOG2E * cc_), (float)opac, xr, yr);
+    }
     if (A.rec64) {
       double* r = A.rec64 + 8 * i;
       r[0] = mx;
@@ -248,6 +262,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.key = (uint64_t*)(frame + L.off_key);
   A.rec32 = (float4*)(frame + L.off_rec32);
   A.rec64 = L.dtype == GSPARC_F64 ? (double*)(frame + L.off_rec64) : nullptr;
+  A.rrec = L.dtype == GSPARC_F32 ? (float4*)(frame + L.off_rrec) : nullptr;
   A.rect = (int4*)(frame + L.off_rect);
   A.counters = (int*)(frame + L.off_counters);
   A.tile_count = (int*)(frame + L.off_tile_count);

@@ -25,6 +25,7 @@ struct BwdArgs {
   const int* tile_start;
   const int* wstop;  // visited prefix per 32-pixel warp (forward AUX pass)
   const float4* rec32;
+  const float4* rrec;  // f32 raster record (f32 frames: same alpha as K4)
   const double* rec64;
   const void* coef;
   const void* dL;  // [B,h,w,C]
@@ -48,6 +49,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   R* s_red = s_coef + NB * CB;           // [NB][6]
   Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6);  // [NB]
   int* s_idx = (int*)(s_rec + NB);       // [NB]
+  float4* s_fr = (float4*)(((uintptr_t)(s_idx + NB) + 15) & ~(uintptr_t)15);  // [NB][2] (f32)
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const int sidx = blockIdx.x, chunk = blockIdx.y;
@@ -95,7 +97,16 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
     if (tid < nb) {
       const uint32_t idx = (uint32_t)A.pairs[start + b0 + tid];
       s_idx[tid] = (int)idx;
-      s_rec[tid] = load_rec_t<R>(A.rec32, A.rec64, idx);
+      if constexpr (sizeof(R) == 4) {
+        // conic recovered from the pre-scaled exponent coefficients
+        const float4 f0 = __ldg(A.rrec + 2 * (size_t)idx), f1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
+        s_fr[2 * tid] = f0;
+        s_fr[2 * tid + 1] = f1;
+        const float k2 = (float)(-2.0 / LOG2E), k1 = (float)(-1.0 / LOG2E);
+        s_rec[tid] = Rec<R>{f0.x, f0.y, f0.z * k2, f0.w * k1, f1.x * k2, f1.y};
+      } else {
+        s_rec[tid] = load_rec_t<R>(A.rec32, A.rec64, idx);
+      }
     }
     for (int e = tid; e < nb * CB; e += blockDim.x) {
       const int j = e / CB, c = e - j * CB;
@@ -110,8 +121,14 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       R wgt = R(0), g_sig = R(0), gc0 = R(0), gc1 = R(0), gc2 = R(0), gm0 = R(0), gm1 = R(0);
       if (k < lastp) {
         const Rec<R> r = s_rec[j];
-        const AlphaOut<R> a =
-            pixel_alpha<R>(pcx, pcy, r.mx, r.my, r.ca, r.cb, r.cc, r.op, wR, half_w);
+        AlphaOut<R> a;
+        if constexpr (sizeof(R) == 4) {
+          const FastAlpha f = fast_alpha_full(pcx, pcy, s_fr[2 * j], s_fr[2 * j + 1], wR,
+                                              1.0f / wR);
+          a = AlphaOut<R>{f.alpha, f.raw, f.g, f.dx, f.dy};
+        } else {
+          a = pixel_alpha<R>(pcx, pcy, r.mx, r.my, r.ca, r.cb, r.cc, r.op, wR, half_w);
+        }
         if (a.alpha > R(0)) {
           const R om = R(1) - a.alpha;
           const R Tb = T / om;
@@ -179,9 +196,9 @@ template <typename R, int CB, int NB>
 static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   const int P = TILE * A.sr;
   const size_t smem_max = sizeof(R) * ((size_t)CB * 256 + (size_t)NB * 256 + NB * CB + NB * 6) +
-                          sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
+                          sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
   const size_t smem = sizeof(R) * ((size_t)CB * P + (size_t)NB * P + NB * CB + NB * 6) +
-                      sizeof(Rec<R>) * NB + sizeof(int) * NB + 16;
+                      sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
   auto kern = k_raster_bwd<R, CB, NB>;
   static bool attr_set = false;  // one per instantiation; keeps capture clean
   if (!attr_set) {
@@ -200,6 +217,7 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.tile_start = (const int*)(frame + L.off_tile_start);
   A.wstop = (const int*)(frame + L.off_wstop);
   A.rec32 = (const float4*)(frame + L.off_rec32);
+  A.rrec = (const float4*)(frame + L.off_rrec);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.coef = frame + L.off_coef;
   A.dL = dL;

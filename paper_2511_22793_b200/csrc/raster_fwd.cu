@@ -312,35 +312,6 @@ static void launch_cfg(const RasterArgs& A, int chunks, cudaStream_t st) {
   kern<<<dim3(A.ntiles * 4, chunks), 256, smem, st>>>(A);
 }
 
-template <bool AUX>
-static int dispatch_f32(const RasterArgs& A, cudaStream_t st) {
-  const int64_t Cp = A.Cp;
-  if (Cp <= 2) {
-    launch_cfg<float, 128, 2, AUX, true, true>(A, 1, st);
-  } else if (Cp <= 4) {
-    launch_cfg<float, 128, 4, AUX, true, true>(A, 1, st);
-  } else {
-    int chunks = (int)((Cp + 127) / 128);
-    int per = (int)((Cp + chunks - 1) / chunks);  // channels per CTA
-    int cc = ((per + 3) / 4 + 3) / 4 * 4;         // per group, multiple of 4
-    if (cc < 4) cc = 4;
-    switch (cc) {
-      case 4: launch_cfg<float, 64, 4, AUX, true, false>(A, chunks, st); break;
-      case 8: launch_cfg<float, 64, 8, AUX, true, false>(A, chunks, st); break;
-      case 12: launch_cfg<float, 64, 12, AUX, true, false>(A, chunks, st); break;
-      case 16: launch_cfg<float, 64, 16, AUX, true, false>(A, chunks, st); break;
-      case 20: launch_cfg<float, 64, 20, AUX, true, false>(A, chunks, st); break;
-      case 24: launch_cfg<float, 64, 24, AUX, true, false>(A, chunks, st); break;
-      case 28: launch_cfg<float, 64, 28, AUX, true, false>(A, chunks, st); break;
-      default: {
-        chunks = (int)((Cp + 127) / 128);
-        launch_cfg<float, 64, 32, AUX, true, false>(A, chunks, st);
-      }
-    }
-  }
-  return GSPARC_OK;
-}
-
 // The raster and its backward split tiles into 4 sub-tiles of 4 rows.
 int forward_sub_rows(const gsparc_frame_layout& /*L*/, int64_t /*Cp*/) { return 4; }
 
@@ -373,9 +344,8 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
               (long long)L.channels);
     return GSPARC_ERR_ARG;
   }
-  // lazy two-pass path for wide channels: tensor-core accumulation
-  if (L.dtype == GSPARC_F32 && A.Cp > 4 && pass != 0)
-    return launch_raster_tc(L, frame, n_tx, C, t_eps, pass, img, st);
+  // f32 frames: one pixel per lane, tcgen05 accumulation (raster_px.cu)
+  if (L.dtype == GSPARC_F32) return launch_raster_px(L, frame, n_tx, C, t_eps, pass, img, st);
   if (pass != 2) {
     if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
       return check_launch("raster live memset");
@@ -393,10 +363,6 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
         else launch_cfg<double, 64, 4, false, true, true>(A, chunks, st);
       }
     }
-  } else {
-    if (pass == 1) launch_cfg<float, 128, 1, true, false, true>(A, 1, st);
-    else if (pass == 0) dispatch_f32<true>(A, st);
-    else dispatch_f32<false>(A, st);
   }
   return check_launch("k_raster");
 }

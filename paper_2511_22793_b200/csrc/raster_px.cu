@@ -1,0 +1,649 @@
+// K4 (f32 frames): front-to-back compositing with one pixel per lane.
+// Replaces do_tile / _tile_alphas (rasterizer.py:169-231).
+//
+// A CTA owns half a 16x16 tile (16 x 8 = 128 pixels, 4 warps of 16 x 2).
+// The tile's depth-ordered list (K3) is consumed in chunks of 32 entries
+// that survive a CTA-level cull: an entry whose alpha >= 1/255 ellipse
+// (rrec.xr/yr, conservative) misses every pixel centre of the CTA has
+// alpha = 0 for all of them, so it multiplies T by exactly 1 and is never
+// included -- skipping it is exact.  Chunks are dense, so the 32 alphas of a
+// chunk are evaluated branch-free with full ILP and a sequential
+// T *= (1 - alpha) per lane (numpy's cumprod order, rasterizer.py:209-212).
+//
+// Pass A (k_pxa): a producer warp scans + culls the list into a shared ring
+//   of chunks (mbarrier full/empty protocol); 4 consumer warps walk them
+//   until every pixel has T < t_eps, writing T_final / count / last, the
+//   per-warp visited prefix (wstop, for K5), the live-Gaussian list, and for
+//   pass B: the chunk's source indices (ch_idx) and every pixel's T at the
+//   start of every chunk (ch_T).  With SC in 1..4 the consumers also
+//   accumulate the image on CUDA cores (fused small-channel path).
+// Pass B (k_pxb): the T checkpoints make chunks independent, so two groups
+//   of 4 weight warps take alternate chunks; each writes its 128 x 32 weight
+//   tile straight into TMEM (tcgen05.st, lane = pixel), two stager warps
+//   write coef^T for the chunk to shared memory (K-major SWIZZLE_128B), and
+//   one thread issues
+//       img[128 px, NP] += W[128, 32] . coef[32, NP]
+//   as tcgen05.mma kind::tf32 with A from TMEM, 3xTF32 split
+//   (Wh.ch + Wh.cl + Wl.ch) for fp32 accuracy, accumulator in TMEM.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gs {
+
+constexpr int PX_K = 32;    // entries per chunk
+constexpr int PX_RING = 4;  // pass-A ring depth (chunks)
+
+struct PxArgs {
+  const uint64_t* pairs;
+  const int* tile_start;
+  const float4* rrec;  // [n][2]
+  const float* coef;   // [n][Cp]
+  uint32_t* ch_idx;    // [slots][32]
+  float* ch_T;         // [slots][128]
+  int* ch_n;           // [2 * ntiles]
+  int* wstop;          // [ntiles * 8]
+  float* T_out;
+  int* count_out;
+  int* last_out;
+  int* live;
+  int* live_list;
+  int* counters;
+  float* img;
+  int64_t Cp;
+  int C, w, h, ntx, ntiles;
+  float t_eps, wf, inv_w;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// First chunk slot of CTA (tile, half): see capi.cu gsparc_plan_frame.
+__device__ __forceinline__ int64_t chunk_slot0(const int* tile_start, int tile, int half) {
+  const int64_t s = tile_start[tile];
+  const int64_t len = tile_start[tile + 1] - s;
+  return 2 * ((s + 31 * (int64_t)tile) >> 5) + half * ((len + 31) >> 5);
+}
+
+struct CtaGeom {
+  int tile, half, x0, y0;
+  float xc, xhalf, ylo, yhi;
+  bool any;
+};
+
+__device__ __forceinline__ CtaGeom cta_geom(const PxArgs& A, int cta) {
+  CtaGeom g;
+  g.tile = cta >> 1;
+  g.half = cta & 1;
+  g.x0 = (g.tile % A.ntx) * TILE;
+  g.y0 = (g.tile / A.ntx) * TILE + g.half * 8;
+  const float xlo = g.x0 + 0.5f, xhi = (float)min(g.x0 + TILE, A.w) - 0.5f;
+  g.ylo = g.y0 + 0.5f;
+  g.yhi = (float)min(g.y0 + 8, A.h) - 0.5f;
+  g.xc = 0.5f * (xlo + xhi);
+  g.xhalf = 0.5f * (xhi - xlo);
+  g.any = g.y0 < A.h;
+  return g;
+}
+
+// Could the entry reach alpha >= 1/255 at any pixel centre of the CTA?
+__device__ __forceinline__ bool cull_keep(float4 r0, float4 r1, const CtaGeom& g, float w,
+                                          float inv_w) {
+  float d = r0.x - g.xc;
+  d = fmaf(-w, rintf(d * inv_w), d);
+  const float dx = fabsf(d) - g.xhalf;
+  const float dy = fmaxf(g.ylo - r0.y, r0.y - g.yhi);
+  return r1.z >= 0.f && dx <= r1.z && dy <= r1.w;
+}
+
+__device__ __forceinline__ void mark_live(const PxArgs& A, int idx) {
+  if (A.live[idx] == 0 && atomicExch(A.live + idx, 1) == 0) {
+    const int pos = atomicAdd(A.counters + GSPARC_CNT_LIVE, 1);
+    A.live_list[pos] = idx;
+  }
+}
+
+// ------------------------------------------------------------------ pass A
+template <int SC>
+__global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
+  constexpr int SCW = SC ? 4 : 1;
+  __shared__ __align__(16) float4 s_ring[PX_RING][PX_K][2];
+  __shared__ __align__(16) float s_cf[PX_RING][PX_K][SCW];
+  __shared__ int s_hdr[PX_RING];
+  __shared__ __align__(8) uint64_t s_full[PX_RING], s_empty[PX_RING];
+  __shared__ int s_ndone, s_nch, s_stop[4];
+
+  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const CtaGeom g = cta_geom(A, blockIdx.x);
+  const int start = A.tile_start[g.tile];
+  const int len = A.tile_start[g.tile + 1] - start;
+  const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PX_RING; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_ndone = 0;
+    s_nch = 0;
+  }
+  if (threadIdx.x < 4) s_stop[threadIdx.x] = 0;
+  __syncthreads();
+
+  if (warp == 4) {
+    // ---------------- producer: scan, cull, compact into the ring
+    const unsigned lt = (1u << lane) - 1u;
+    int c = 0, fill = 0, acquired = 0;
+    auto acquire = [&](int k) {
+      if (k > acquired) {
+        if (k >= PX_RING) mbar_wait(&s_empty[k % PX_RING], ((k / PX_RING) - 1) & 1);
+        acquired = k;
+      }
+    };
+    auto publish = [&](int k, int n) {
+      __syncwarp();
+      if (lane == 0) {
+        s_hdr[k % PX_RING] = n;
+        mbar_arrive(&s_full[k % PX_RING]);
+      }
+    };
+    const int end = g.any ? len : 0;
+    // software pipeline: pairs of batch b+1 and records of batch b in flight
+    uint32_t idx_n = 0xffffffffu;
+    if (lane < end) idx_n = (uint32_t)__ldg(A.pairs + start + lane);
+    for (int pos = 0; pos < end; pos += 32) {
+      const uint32_t idx = idx_n;
+      float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+      if (idx != 0xffffffffu) {
+        r0 = __ldg(A.rrec + 2 * (size_t)idx);
+        r1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
+      }
+      idx_n = 0xffffffffu;
+      if (pos + 32 + lane < end) idx_n = (uint32_t)__ldg(A.pairs + start + pos + 32 + lane);
+      if (*(volatile int*)&s_ndone == 4) break;  // every pixel finished
+      const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const int ns = __popc(m);
+      acquire(c);
+      if (fill + ns > PX_K) acquire(c + 1);
+      if (keep) {
+        const int q = fill + __popc(m & lt);
+        const int k = q < PX_K ? c : c + 1;
+        const int e = q & (PX_K - 1);
+        s_ring[k % PX_RING][e][0] = r0;
+        s_ring[k % PX_RING][e][1] =
+            make_float4(r1.x, r1.y, __int_as_float(pos + lane), __int_as_float((int)idx));
+        if (SC) {
+#pragma unroll
+          for (int ch = 0; ch < SCW; ++ch)
+            s_cf[k % PX_RING][e][ch] = ch < SC ? __ldg(A.coef + (int64_t)idx * SC + ch) : 0.f;
+        }
+        A.ch_idx[(slot0 + k) * PX_K + e] = idx;
+      }
+      fill += ns;
+      if (fill >= PX_K) {
+        publish(c, PX_K);
+        ++c;
+        fill -= PX_K;
+      }
+    }
+    if (fill > 0) {  // zero-opacity padding: alpha = 0, never included
+      if (lane >= fill) {
+        s_ring[c % PX_RING][lane][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        s_ring[c % PX_RING][lane][1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+        if (SC) {
+#pragma unroll
+          for (int ch = 0; ch < SCW; ++ch) s_cf[c % PX_RING][lane][ch] = 0.f;
+        }
+        A.ch_idx[(slot0 + c) * PX_K + lane] = 0xffffffffu;
+      }
+      publish(c, fill);
+      ++c;
+    }
+    acquire(c);
+    publish(c, -1);  // end of list
+  } else {
+    // ---------------- consumers: one pixel per lane
+    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * warp + (lane >> 4);
+    const bool inside = px < A.w && py < A.h;
+    const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
+    const float teps = A.t_eps, wf = A.wf, inv_w = A.inv_w;
+    float T = inside ? 1.f : 0.f;  // outside pixels are never live
+    int cnt = 0, last = 0, lastch = 0;
+    float acc[SCW];
+#pragma unroll
+    for (int ch = 0; ch < SCW; ++ch) acc[ch] = 0.f;
+    bool wdone = !__any_sync(0xffffffffu, T >= teps);
+    if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
+    for (int c = 0;; ++c) {
+      const int s = c % PX_RING;
+      mbar_wait(&s_full[s], (c / PX_RING) & 1);
+      const int n = *(volatile int*)&s_hdr[s];
+      if (n < 0) break;
+      A.ch_T[(slot0 + c) * 128 + warp * 32 + lane] = T;  // checkpoint for pass B
+      if (!wdone) {
+        unsigned actm = 0;
+        float Tl = T;
+#pragma unroll
+        for (int k = 0; k < PX_K; ++k) {
+          const float4 r0 = s_ring[s][k][0], r1 = s_ring[s][k][1];
+          const float a = fast_alpha(pcx, pcy, r0, r1, wf, inv_w);
+          const bool act = Tl >= teps && a > 0.f;
+          if (SC) {
+            const float wgt = act ? Tl * a : 0.f;
+            const float4 cf = *(const float4*)&s_cf[s][k][0];
+            acc[0] = fmaf(wgt, cf.x, acc[0]);
+            if (SC > 1) acc[1] = fmaf(wgt, cf.y, acc[1]);
+            if (SC > 2) acc[2] = fmaf(wgt, cf.z, acc[2]);
+            if (SC > 3) acc[3] = fmaf(wgt, cf.w, acc[3]);
+          }
+          Tl = act ? Tl * (1.f - a) : Tl;
+          actm |= act ? (1u << k) : 0u;
+        }
+        T = Tl;
+        if (actm) {
+          cnt += __popc(actm);
+          last = __float_as_int(s_ring[s][31 - __clz(actm)][1].z) + 1;
+        }
+        const unsigned um = __reduce_or_sync(0xffffffffu, actm);
+        if (um) {
+          lastch = c + 1;
+          if ((um >> lane) & 1u) mark_live(A, __float_as_int(s_ring[s][lane][1].w));
+        }
+        wdone = !__any_sync(0xffffffffu, T >= teps);
+        if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[s]);
+    }
+    if (inside) {
+      const int q = py * A.w + px;
+      A.T_out[q] = inside ? T : 1.f;
+      A.count_out[q] = cnt;
+      A.last_out[q] = last;
+      if (SC) {
+#pragma unroll
+        for (int ch = 0; ch < SC; ++ch) {
+          const int b = ch / A.C, cc = ch - b * A.C;
+          A.img[(((int64_t)b * A.h + py) * A.w + px) * A.C + cc] = acc[ch];
+        }
+      }
+    }
+    const int wmax = __reduce_max_sync(0xffffffffu, last);
+    if (lane == 0) {
+      A.wstop[g.tile * 8 + g.half * 4 + warp] = wmax;
+      atomicMax(&s_nch, lastch);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) A.ch_n[blockIdx.x] = s_nch;
+}
+
+// ------------------------------------------------------------------ pass B
+// K-major SWIZZLE_128B UMMA descriptor: rows of 128 B, 8-row atoms 1024 B
+// apart (SBO), LBO unused, version 1, layout type 2.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// byte offset of element (row r, k) of a [rows][32] f32 K-major SW128 tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
+  return (uint32_t)(r * 128 + ((((k >> 2) ^ (r & 7)) << 4) | ((k & 3) << 2)));
+}
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]));
+}
+
+constexpr int PXB_THREADS = 352;  // 8 weight warps, 2 stager warps, 1 MMA warp
+
+template <int NP>
+__global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
+  constexpr uint32_t ACC_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  constexpr uint32_t TMEM_COLS = ACC_COLS + 128 <= 256 ? 256 : 512;
+  constexpr int B_BYTES = NP * 128;         // one operand copy (hi or lo)
+  constexpr int STAGE = 2 * B_BYTES;        // hi + lo
+  constexpr int NH = NP / 2;                // channels per stager warp
+  static_assert(NP % 8 == 0 && NP <= 256, "NP");
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sB = sm;                                    // [2 stages][hi|lo]
+  float4* s_rec = (float4*)(sm + 2 * STAGE);                 // [8 warps][32][2]
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_done;
+  __shared__ uint32_t s_tmem;
+
+  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const CtaGeom g = cta_geom(A, blockIdx.x);
+  const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
+  const int nch = g.any ? A.ch_n[blockIdx.x] : 0;
+  const int col0 = blockIdx.y * NP;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&s_full[0], 6);
+    mbar_init(&s_full[1], 6);
+    mbar_init(&s_empty[0], 1);
+    mbar_init(&s_empty[1], 1);
+    mbar_init(&s_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 10) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  // operands must be finite: zero both B stages once (entries past a
+  // chunk's end then meet zero weights, never NaN garbage)
+  for (int i = threadIdx.x; i < 2 * STAGE / 16; i += blockDim.x)
+    ((float4*)sB)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+
+  if (warp < 8) {
+    // ---------------- weight warps: group gq takes chunks c = gq (mod 2)
+    const int gq = warp >> 2, q = warp & 3;
+    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
+    const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
+    const float teps = A.t_eps, wf = A.wf, inv_w = A.inv_w;
+    float4* rs = s_rec + warp * 64;
+    const uint32_t a_hi = tmem + ((uint32_t)(32 * q) << 16) + ACC_COLS + 64 * gq;
+    const uint32_t a_lo = a_hi + 32;
+    for (int c = gq; c < nch; c += 2) {
+      const int k = c >> 1;
+      const int64_t slot = slot0 + c;
+      const uint32_t idx = A.ch_idx[slot * PX_K + lane];
+      float T = A.ch_T[slot * 128 + q * 32 + lane];
+      float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+      if (idx != 0xffffffffu) {
+        r0 = __ldg(A.rrec + 2 * (size_t)idx);
+        r1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
+      }
+      __syncwarp();  // previous chunk's readers are done with rs
+      rs[2 * lane] = r0;
+      rs[2 * lane + 1] = r1;
+      __syncwarp();
+      float wv[PX_K];
+      if (__any_sync(0xffffffffu, T >= teps)) {
+#pragma unroll
+        for (int e = 0; e < PX_K; ++e) {
+          const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
+          const bool act = T >= teps && a > 0.f;
+          wv[e] = act ? T * a : 0.f;
+          T = act ? T * (1.f - a) : T;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
+      }
+      if (k >= 1) mbar_wait(&s_empty[gq], (k - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float v = wv[16 * hh + j];
+          const uint32_t hb = __float_as_uint(v) & 0xFFFFE000u;
+          hi[j] = hb;
+          lo[j] = __float_as_uint(v - __uint_as_float(hb));
+        }
+        tmem_st16(a_hi + 16 * hh, hi);
+        tmem_st16(a_lo + 16 * hh, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_full[gq]);
+    }
+  } else if (warp < 10) {
+    // ---------------- stagers: coef^T of the chunk -> B (K-major SW128)
+    // lane = chunk entry (row of coef), channels in blocks of SB registers
+    constexpr int SB = NH <= 64 ? NH : 32;
+    const int h0 = (warp - 8) * NH;  // first channel of this warp
+    const bool vec = (A.Cp & 3) == 0;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c & 1, k = c >> 1;
+      const uint32_t idx = A.ch_idx[(slot0 + c) * PX_K + lane];
+      unsigned char* bhi = sB + s * STAGE;
+      unsigned char* blo = bhi + B_BYTES;
+#pragma unroll 1
+      for (int jb = 0; jb < NH; jb += SB) {
+        float v[SB];
+        const int64_t cb = col0 + h0 + jb;
+        const float* row = A.coef + (int64_t)idx * A.Cp + cb;
+        const int64_t rem = A.Cp - cb;
+        const int nv = rem < SB ? (int)rem : SB;
+        if (idx == 0xffffffffu || nv <= 0) {
+#pragma unroll
+          for (int j = 0; j < SB; ++j) v[j] = 0.f;
+        } else if (vec && nv == SB) {
+#pragma unroll
+          for (int j = 0; j < SB; j += 4) {
+            const float4 t = __ldg((const float4*)(row + j));
+            v[j] = t.x;
+            v[j + 1] = t.y;
+            v[j + 2] = t.z;
+            v[j + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < SB; ++j) v[j] = j < nv ? __ldg(row + j) : 0.f;
+        }
+        if (jb == 0 && k >= 1) mbar_wait(&s_empty[s], (k - 1) & 1);
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+          const float hv = __uint_as_float(__float_as_uint(v[j]) & 0xFFFFE000u);
+          const uint32_t off = sw128_off(h0 + jb + j, lane);
+          *(float*)(bhi + off) = hv;
+          *(float*)(blo + off) = v[j] - hv;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_full[s]);
+    }
+  } else if (lane == 0) {
+    // ---------------- MMA issuer
+    // instruction descriptor: D f32, A/B tf32, K-major, N = NP, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+    for (int c = 0; c < nch; ++c) {
+      const int s = c & 1, k = c >> 1;
+      mbar_wait(&s_full[s], k & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a_hi = tmem + ACC_COLS + 64 * s, a_lo = a_hi + 32;
+      const uint32_t b_hi = smem_u32(sB + s * STAGE), b_lo = b_hi + B_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < PX_K / 8; ++ks) {
+        const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
+        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_sw128(b_hi + 32 * ks), idesc, acc0);
+        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_sw128(b_lo + 32 * ks), idesc, 1u);
+        mma_tf32_ts(tmem, a_lo + 8 * ks, umma_desc_sw128(b_hi + 32 * ks), idesc, 1u);
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(&s_empty[s]))
+          : "memory");
+    }
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&s_done))
+        : "memory");
+  }
+
+  // ---------------- epilogue: warps 0..3 own TMEM lanes 32q.. (= pixels)
+  if (warp < 4) {
+    const int q = warp;
+    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
+    const bool inside = px < A.w && py < A.h;
+    if (nch > 0) {
+      mbar_wait(&s_done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NP; c0 += 8) {
+      uint32_t v[8];
+      if (nch > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0u;
+      }
+      const int64_t cc0 = col0 + c0;
+      if (!inside || cc0 >= A.Cp) continue;
+      if (fast) {
+        const int64_t b = cc0 / A.C, ch = cc0 - b * A.C;
+        float4* dst = (float4*)(A.img + ((b * A.h + py) * (int64_t)A.w + px) * A.C + ch);
+        dst[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                             __uint_as_float(v[3]));
+        dst[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]),
+                             __uint_as_float(v[7]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t cc = cc0 + j;
+          if (cc < A.Cp) {
+            const int64_t b = cc / A.C, ch = cc - b * A.C;
+            A.img[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch] = __uint_as_float(v[j]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 10) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+template <int NP>
+static void launch_pxb(const PxArgs& A, int chunks_y, cudaStream_t st) {
+  constexpr int STAGE = 2 * NP * 128;
+  // >= 80 KB keeps residency at two CTAs per SM (the TMEM budget)
+  size_t smem = 2 * STAGE + 8 * 64 * 16 + 1024;
+  if (smem < 80 * 1024) smem = 80 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_pxb<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_pxb<NP><<<dim3(A.ntiles * 2, chunks_y), PXB_THREADS, smem, st>>>(A);
+}
+
+static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
+                           double t_eps, void* img) {
+  PxArgs A;
+  A.pairs = (const uint64_t*)(frame + L.off_pairs);
+  A.tile_start = (const int*)(frame + L.off_tile_start);
+  A.rrec = (const float4*)(frame + L.off_rrec);
+  A.coef = (const float*)(frame + L.off_coef);
+  A.ch_idx = (uint32_t*)(frame + L.off_ch_idx);
+  A.ch_T = (float*)(frame + L.off_ch_T);
+  A.ch_n = (int*)(frame + L.off_ch_n);
+  A.wstop = (int*)(frame + L.off_wstop);
+  A.T_out = (float*)(frame + L.off_T);
+  A.count_out = (int*)(frame + L.off_count);
+  A.last_out = (int*)(frame + L.off_last);
+  A.live = (int*)(frame + L.off_live);
+  A.live_list = (int*)(frame + L.off_live_list);
+  A.counters = (int*)(frame + L.off_counters);
+  A.img = (float*)img;
+  A.Cp = (int64_t)n_tx * C;
+  A.C = C;
+  A.w = L.width;
+  A.h = L.height;
+  A.ntx = L.ntx;
+  A.ntiles = L.ntiles;
+  A.t_eps = (float)t_eps;
+  A.wf = (float)L.width;
+  A.inv_w = 1.0f / (float)L.width;
+  return A;
+}
+
+// pass 1: weights only (aux, live list, chunk lists), any Cp
+// pass 0: fused; Cp <= 4 accumulates in pass A, wider runs A then B
+// pass 2: accumulation only (after pass 1 and the MLP)
+int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C, double t_eps,
+                     int pass, void* img, cudaStream_t st) {
+  PxArgs A = make_px_args(L, frame, n_tx, C, t_eps, img);
+  const int64_t Cp = A.Cp;
+  if (pass != 2) {
+    if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
+      return check_launch("raster live memset");
+    const int grid = L.ntiles * 2;
+    if (pass == 0 && Cp <= 4) {
+      switch (Cp) {
+        case 1: k_pxa<1><<<grid, 160, 0, st>>>(A); break;
+        case 2: k_pxa<2><<<grid, 160, 0, st>>>(A); break;
+        case 3: k_pxa<3><<<grid, 160, 0, st>>>(A); break;
+        default: k_pxa<4><<<grid, 160, 0, st>>>(A); break;
+      }
+      return check_launch("k_pxa");
+    }
+    k_pxa<0><<<grid, 160, 0, st>>>(A);
+    GS_TRY(check_launch("k_pxa"));
+    if (pass == 1) return GSPARC_OK;
+  }
+  const int chunks = (int)((Cp + 255) / 256);
+  const int64_t per = (Cp + chunks - 1) / chunks;
+  if (per <= 32) launch_pxb<32>(A, chunks, st);
+  else if (per <= 64) launch_pxb<64>(A, chunks, st);
+  else if (per <= 104) launch_pxb<104>(A, chunks, st);
+  else if (per <= 128) launch_pxb<128>(A, chunks, st);
+  else launch_pxb<256>(A, chunks, st);
+  return check_launch("k_pxb");
+}
+
+}  // namespace gs

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.gsparc_abi_version() == 1
+    assert L.gsparc_abi_version() == 2
 
 
 def test_plan_frame_layout(L):
@@ -48,11 +48,14 @@ def test_plan_frame_layout(L):
     assert rc == 0
     assert (lay.ntx, lay.nty, lay.ntiles) == (23, 6, 138)
     offs = [getattr(lay, "off_" + k) for k in _lib._LAYOUT_OFFSETS
-            if k != "rec64"]
+            if k not in ("rec64", "pair_rec")]
     assert all(o % 256 == 0 for o in offs)
     assert len(set(offs)) == len(offs)
     assert lay.total_bytes >= lay.off_ggeo + 4096 * 8 * 4
     assert lay.off_pairs + 8 * 200000 <= lay.total_bytes
+    # chunk slots bound the CTA chunk lists of any pair layout
+    assert lay.ch_slots >= 2 * (200000 + 31 * 138) // 32
+    assert lay.off_ch_T + 4 * 128 * lay.ch_slots <= lay.total_bytes
 
 
 def test_plan_frame_rejects_bad_args(L):
