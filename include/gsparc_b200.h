@@ -127,7 +127,11 @@ typedef struct gsparc_frame_layout {
   int64_t off_ch_T;       /* f32  [slots,128] transmittance of the CTA's
                              128 pixels at the start of every chunk       */
   int64_t off_ch_n;       /* i32  [2*ntiles] chunks with a contribution   */
+  int64_t off_ch_rec;     /* f32  [slots,32,8] chunk entry records
+                             {mx,my,qa,qb,qc,opacity,list pos,index}      */
   int64_t ch_slots;       /* chunk slots (>= 2*(pairs+31*ntiles)/32 + 2) */
+  int64_t off_ch_used;    /* u32  [slots] entries of a chunk with at least
+                             one included contribution in the CTA        */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

@@ -41,7 +41,7 @@ _LAYOUT_OFFSETS = ("key", "rec32", "rec64", "rect", "counters", "tile_count",
                    "tile_cursor", "tile_start", "tile_stop", "pairs", "T",
                    "count", "last", "live", "live_list", "coef", "gcoef",
                    "ggeo", "pair_rec", "wstop", "rrec", "ch_idx", "ch_T",
-                   "ch_n")
+                   "ch_n", "ch_rec")
 
 
 class CLayout(ctypes.Structure):
@@ -50,7 +50,7 @@ class CLayout(ctypes.Structure):
                 [(k, c_i32) for k in ("width", "height", "ntx", "nty", "ntiles",
                                       "dtype", "with_backward", "reserved")] +
                 [("off_" + k, c_i64) for k in _LAYOUT_OFFSETS] +
-                [("ch_slots", c_i64)])
+                [("ch_slots", c_i64), ("off_ch_used", c_i64)])
 
 
 class CAdamConfig(ctypes.Structure):

@@ -81,11 +81,26 @@ static int check_frame(const void* frame, const gsparc_frame_layout* L) {
 
 }  // namespace gs
 
+namespace gs {
+extern long long* gsparc_dbg_ptr;
+}
+
 using namespace gs;
 
 extern "C" {
 
 int gsparc_abi_version(void) { return GSPARC_ABI_VERSION; }
+
+// experiments only (not in the public header): device pointer of the last
+// pass-B timing buffer when GSPARC_PXB_DBG is set
+void* gsparc_debug_timing(void) { return (void*)gs::gsparc_dbg_ptr; }
+int gsparc_debug_copy(long long* host, int64_t count) {
+  if (!gs::gsparc_dbg_ptr) return GSPARC_ERR_ARG;
+  return cudaMemcpy(host, gs::gsparc_dbg_ptr, sizeof(long long) * count, cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? GSPARC_OK
+             : GSPARC_ERR_CUDA;
+}
 
 const char* gsparc_last_error(void) { return g_err; }
 
@@ -150,6 +165,8 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_ch_idx = take(dtype == GSPARC_F32 ? 4 * 32 * L.ch_slots : 0);
   L.off_ch_T = take(dtype == GSPARC_F32 ? 4 * 128 * L.ch_slots : 0);
   L.off_ch_n = take(sizeof(int) * 2 * L.ntiles);
+  L.off_ch_rec = take(dtype == GSPARC_F32 ? 32 * 32 * L.ch_slots : 0);
+  L.off_ch_used = take(dtype == GSPARC_F32 ? 4 * L.ch_slots : 0);
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

@@ -24,7 +24,8 @@ struct MlpArgs {
   const float4* rec32;
   const double* rec64;
   const uint64_t* key;
-  const int* live_list;  // nullptr -> all Gaussians (culled skipped)
+  const int* live;       // live flags (K4 pass A); nullptr -> all kept
+  int* counters_rw;      // CNT_LIVE is counted here when `live` is set
   const int* counters;
   void* coef;
   int64_t n;
@@ -43,10 +44,16 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gi = t / A.B;
   const int b = (int)(t % A.B);
-  int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
-  if (gi >= count) return;
-  const int64_t i = A.live_list ? A.live_list[gi] : gi;
-  if (!A.live_list && A.key[i] == ~0ULL) return;
+  if (gi >= A.n) return;
+  const int64_t i = gi;
+  if (A.live) {
+    const bool lv = A.live[i] != 0;
+    const unsigned m = __ballot_sync(__activemask(), lv && b == 0);
+    if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(A.counters_rw + GSPARC_CNT_LIVE, __popc(m));
+    if (!lv) return;
+  } else if (A.key[i] == ~0ULL) {
+    return;
+  }
   R theta, phi;
   if constexpr (sizeof(R) == 4) {
     float4 r = A.rec32[2 * i + 1];
@@ -72,7 +79,8 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
     const float* w2 = w + H * I + H;
     const float* b2 = w2 + C * H;
     double d = tx_distance(A.pos + 3 * i, txb);
-    float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+    const int64_t o0 = i * A.Cp + (int64_t)b * C;
+    float* out = (float*)A.coef + o0;
     for (int c = 0; c < C; ++c) {
       float acc = 0.f;
       for (int h = 0; h < H; ++h) acc += w2[c * H + h] * hid32[h];
@@ -100,21 +108,32 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
   }
 }
 
-// Wide head, f32 weights, H == 16, I == 5, C % 4 == 0.
+// Wide head, f32 weights, H == 16, I == 5, C % 4 == 0, C <= 128.
+// Every load of the Gaussian (its W1/b1 row, all of W2 and b2, theta/phi)
+// is issued before any arithmetic, so one warp has ~7.5 KB in flight and
+// pays a single memory latency per Gaussian.
 __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int lane) {
-  const float4 r1 = A.rec32[2 * i + 1];
+  constexpr int MAXV = 16;  // 4C/32 float4 per lane (C <= 128)
   const float* w = A.w32 + i * (int64_t)A.P;
   const int C = A.C;
-  // W1 row for hidden unit `lane & 15`
+  const int nvec = 4 * C;
   const int hu = lane & 15;
+  const float4 r1 = __ldg(A.rec32 + 2 * i + 1);
   float w1[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) w1[k] = __ldg(w + hu * 5 + k);
   const float b1 = __ldg(w + 80 + hu);
   const float4* w2v = reinterpret_cast<const float4*>(w + 96);
   const float* b2 = w + 96 + 16 * C;
+  float4 v[MAXV];
+  float bv[MAXV];
+#pragma unroll
+  for (int u = 0; u < MAXV; ++u) {
+    const int f = u * 32 + lane;
+    v[u] = f < nvec ? __ldg(w2v + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bv[u] = (f < nvec && (lane & 3) == 0) ? __ldg(b2 + (f >> 2)) : 0.f;
+  }
   const int q = lane & 3;
-  const int nvec = 4 * C;
   const double* p = A.pos + 3 * i;
   for (int b = 0; b < A.B; ++b) {
     const double* txb = A.tx + 3 * b;
@@ -123,47 +142,59 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
 #pragma unroll
     for (int k = 0; k < 5; ++k) pre += w1[k] * x[k];
     pre += b1;
-    float hid = pre > 0.f ? pre : 0.f;
-    float h0 = __shfl_sync(0xffffffffu, hid, 4 * q + 0);
-    float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
-    float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
-    float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
+    const float hid = pre > 0.f ? pre : 0.f;
+    const float h0 = __shfl_sync(0xffffffffu, hid, 4 * q + 0);
+    const float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
+    const float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
+    const float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
     const double d = tx_distance(p, txb);
     float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
-    // issue every W2 load of this lane before using any (latency overlap)
-    constexpr int MAXV = 16;  // 4C/32 float4 per lane, C <= 128 per pass
-    for (int f0 = 0; f0 < nvec; f0 += 32 * MAXV) {
-      float4 v[MAXV];
 #pragma unroll
-      for (int u = 0; u < MAXV; ++u) {
-        const int f = f0 + u * 32 + lane;
-        v[u] = f < nvec ? __ldg(w2v + f) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < MAXV; ++u) {
-        const int f = f0 + u * 32 + lane;
-        if (f0 + u * 32 >= nvec) break;
-        float part = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if (q == 0 && f < nvec) {
-          const int o = f >> 2;
-          out[o] = (float)((double)(part + __ldg(b2 + o)) / d);
-        }
-      }
+    for (int u = 0; u < MAXV; ++u) {
+      if (u * 32 >= nvec) break;
+      const int f = u * 32 + lane;
+      float part = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (q == 0 && f < nvec) out[f >> 2] = (float)((double)(part + bv[u]) / d);
     }
   }
 }
 
 __global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
   const int lane = threadIdx.x & 31;
-  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < count;
-       gi += nwarps) {
-    const int64_t i = A.live_list ? A.live_list[gi] : gi;
-    if (!A.live_list && A.key[i] == ~0ULL) continue;
-    mlp_wide_one(A, i, lane);
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (A.live) {
+    // CTA-level compaction of 256 live flags, then warps take the live
+    // Gaussians round robin (balances the Poisson spread of live flags)
+    __shared__ int s_list[256];
+    __shared__ int s_wc[8], s_n;
+    const int warp = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const bool lv = j < A.n && A.live[j] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, lv);
+    if (lane == 0) s_wc[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int k = 0; k < 8; ++k) {
+        const int c = s_wc[k];
+        s_wc[k] = run;
+        run += c;
+      }
+      s_n = run;
+      if (run) atomicAdd(A.counters_rw + GSPARC_CNT_LIVE, run);
+    }
+    __syncthreads();
+    if (lv) s_list[s_wc[warp] + __popc(m & ((1u << lane) - 1u))] = (int)j;
+    __syncthreads();
+    for (int k = warp; k < s_n; k += 8) mlp_wide_one(A, s_list[k], lane);
+    return;
+  }
+  for (int64_t gi = wid; gi < A.n; gi += nwarps) {
+    if (A.key[gi] == ~0ULL) continue;
+    mlp_wide_one(A, gi, lane);
   }
 }
 
@@ -177,7 +208,8 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
   A.rec32 = (const float4*)(frame + L.off_rec32);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.key = (const uint64_t*)(frame + L.off_key);
-  A.live_list = live_only ? (const int*)(frame + L.off_live_list) : nullptr;
+  A.live = live_only ? (const int*)(frame + L.off_live) : nullptr;
+  A.counters_rw = (int*)(frame + L.off_counters);
   A.counters = (const int*)(frame + L.off_counters);
   A.coef = frame + L.off_coef;
   A.n = cloud.n;
@@ -205,10 +237,10 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     }
     int64_t threads = cloud.n * B;
     k_mlp_narrow<double><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
-  } else if (A.C % 4 == 0 && A.C >= 16 && A.H == 16 && A.I == 5) {
+  } else if (A.C % 4 == 0 && A.C >= 16 && A.C <= 128 && A.H == 16 && A.I == 5) {
     int64_t threads = cloud.n * 32;
     int64_t blocks = (threads + 255) / 256;
-    if (live_only && blocks > 148 * 8) blocks = 148 * 8;  // grid-stride over the live list
+    if (live_only) blocks = (cloud.n + 255) / 256;  // a CTA per 256 live flags
     k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
   } else {
     int64_t threads = cloud.n * B;

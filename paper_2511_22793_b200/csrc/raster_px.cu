@@ -25,6 +25,10 @@
 //       img[128 px, NP] += W[128, 32] . coef[32, NP]
 //   as tcgen05.mma kind::tf32 with A from TMEM, 3xTF32 split
 //   (Wh.ch + Wh.cl + Wl.ch) for fp32 accuracy, accumulator in TMEM.
+#include <cuda.h>
+#include <stdlib.h>
+#include <string.h>  // CUtensorMap (encoded through the runtime's driver entry point)
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -38,7 +42,10 @@ struct PxArgs {
   const int* tile_start;
   const float4* rrec;  // [n][2]
   const float* coef;   // [n][Cp]
+  uint32_t* ch_used;   // [slots] CTA-level included-entry mask per chunk
+  long long* dbg;      // optional per-CTA timing counters (experiments)
   uint32_t* ch_idx;    // [slots][32]
+  float4* ch_rec;      // [slots][32][2]
   float* ch_T;         // [slots][128]
   int* ch_n;           // [2 * ntiles]
   int* wstop;          // [ntiles * 8]
@@ -49,7 +56,7 @@ struct PxArgs {
   int* live_list;
   int* counters;
   float* img;
-  int64_t Cp;
+  int64_t Cp, n;
   int C, w, h, ntx, ntiles;
   float t_eps, wf, inv_w;
 };
@@ -74,6 +81,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// Same wait with a sleeping back-off: many warps polling mbarriers flood
+// the shared-memory (MIO) pipe that the producers' copies also need.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
 }
 
 // First chunk slot of CTA (tile, half): see capi.cu gsparc_plan_frame.
@@ -112,13 +135,6 @@ __device__ __forceinline__ bool cull_keep(float4 r0, float4 r1, const CtaGeom& g
   const float dx = fabsf(d) - g.xhalf;
   const float dy = fmaxf(g.ylo - r0.y, r0.y - g.yhi);
   return r1.z >= 0.f && dx <= r1.z && dy <= r1.w;
-}
-
-__device__ __forceinline__ void mark_live(const PxArgs& A, int idx) {
-  if (A.live[idx] == 0 && atomicExch(A.live + idx, 1) == 0) {
-    const int pos = atomicAdd(A.counters + GSPARC_CNT_LIVE, 1);
-    A.live_list[pos] = idx;
-  }
 }
 
 // ------------------------------------------------------------------ pass A
@@ -162,23 +178,45 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     auto publish = [&](int k, int n) {
       __syncwarp();
       if (lane == 0) {
+        if (n > 0) A.ch_used[slot0 + k] = 0u;  // consumers OR their masks in
         s_hdr[k % PX_RING] = n;
         mbar_arrive(&s_full[k % PX_RING]);
       }
     };
     const int end = g.any ? len : 0;
-    // software pipeline: pairs of batch b+1 and records of batch b in flight
-    uint32_t idx_n = 0xffffffffu;
-    if (lane < end) idx_n = (uint32_t)__ldg(A.pairs + start + lane);
-    for (int pos = 0; pos < end; pos += 32) {
-      const uint32_t idx = idx_n;
-      float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-      if (idx != 0xffffffffu) {
-        r0 = __ldg(A.rrec + 2 * (size_t)idx);
-        r1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
+    // software pipeline: list indices DI batches ahead, records DR batches
+    // ahead (the record load depends on the index load)
+    constexpr int DI = 6, DR = 3;
+    auto ld_idx = [&](int p) -> uint32_t {
+      return p + lane < end ? (uint32_t)__ldg(A.pairs + start + p + lane) : 0xffffffffu;
+    };
+    auto ld_rec = [&](uint32_t i, float4& a, float4& b) {
+      if (i != 0xffffffffu) {
+        a = __ldg(A.rrec + 2 * (size_t)i);
+        b = __ldg(A.rrec + 2 * (size_t)i + 1);
+      } else {
+        a = make_float4(0.f, 0.f, 0.f, 0.f);
+        b = make_float4(0.f, 0.f, -1.f, -1.f);
       }
-      idx_n = 0xffffffffu;
-      if (pos + 32 + lane < end) idx_n = (uint32_t)__ldg(A.pairs + start + pos + 32 + lane);
+    };
+    uint32_t qi[DI];
+    float4 qa[DR], qb[DR];
+#pragma unroll
+    for (int j = 0; j < DI; ++j) qi[j] = ld_idx(32 * j);
+#pragma unroll
+    for (int j = 0; j < DR; ++j) ld_rec(qi[j], qa[j], qb[j]);
+    for (int pos = 0; pos < end; pos += 32) {
+      const uint32_t idx = qi[0];
+      const float4 r0 = qa[0], r1 = qb[0];
+#pragma unroll
+      for (int j = 0; j + 1 < DR; ++j) {
+        qa[j] = qa[j + 1];
+        qb[j] = qb[j + 1];
+      }
+      ld_rec(qi[DR], qa[DR - 1], qb[DR - 1]);
+#pragma unroll
+      for (int j = 0; j + 1 < DI; ++j) qi[j] = qi[j + 1];
+      qi[DI - 1] = ld_idx(pos + 32 * DI);
       if (*(volatile int*)&s_ndone == 4) break;  // every pixel finished
       const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -189,15 +227,19 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         const int q = fill + __popc(m & lt);
         const int k = q < PX_K ? c : c + 1;
         const int e = q & (PX_K - 1);
-        s_ring[k % PX_RING][e][0] = r0;
-        s_ring[k % PX_RING][e][1] =
+        const float4 r1p =
             make_float4(r1.x, r1.y, __int_as_float(pos + lane), __int_as_float((int)idx));
+        s_ring[k % PX_RING][e][0] = r0;
+        s_ring[k % PX_RING][e][1] = r1p;
         if (SC) {
 #pragma unroll
           for (int ch = 0; ch < SCW; ++ch)
             s_cf[k % PX_RING][e][ch] = ch < SC ? __ldg(A.coef + (int64_t)idx * SC + ch) : 0.f;
         }
-        A.ch_idx[(slot0 + k) * PX_K + e] = idx;
+        const int64_t o = (slot0 + k) * PX_K + e;
+        A.ch_idx[o] = idx;
+        A.ch_rec[2 * o] = r0;
+        A.ch_rec[2 * o + 1] = r1p;
       }
       fill += ns;
       if (fill >= PX_K) {
@@ -214,7 +256,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
 #pragma unroll
           for (int ch = 0; ch < SCW; ++ch) s_cf[c % PX_RING][lane][ch] = 0.f;
         }
-        A.ch_idx[(slot0 + c) * PX_K + lane] = 0xffffffffu;
+        const int64_t o = (slot0 + c) * PX_K + lane;
+        A.ch_idx[o] = 0xffffffffu;
+        A.ch_rec[2 * o] = make_float4(0.f, 0.f, 0.f, 0.f);
+        A.ch_rec[2 * o + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
       }
       publish(c, fill);
       ++c;
@@ -267,7 +312,9 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         const unsigned um = __reduce_or_sync(0xffffffffu, actm);
         if (um) {
           lastch = c + 1;
-          if ((um >> lane) & 1u) mark_live(A, __float_as_int(s_ring[s][lane][1].w));
+          if (lane == 0) atomicOr(A.ch_used + slot0 + c, um);
+          // fire-and-forget flag; the MLP compacts the flags itself
+          if ((um >> lane) & 1u) A.live[__float_as_int(s_ring[s][lane][1].w)] = 1;
         }
         wdone = !__any_sync(0xffffffffu, T >= teps);
         if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
@@ -311,11 +358,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// byte offset of element (row r, k) of a [rows][32] f32 K-major SW128 tile
-__device__ __forceinline__ uint32_t sw128_off(int r, int k) {
-  return (uint32_t)(r * 128 + ((((k >> 2) ^ (r & 7)) << 4) | ((k & 3) << 2)));
-}
-
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -334,24 +376,68 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       "r"(v[15]));
 }
 
-constexpr int PXB_THREADS = 352;  // 8 weight warps, 2 stager warps, 1 MMA warp
+// Pass B:  img[128 px, NP] += W[128 px, 32] . coef[32, NP] per chunk.
+//   A = W (tf32 hi/lo) in TMEM, lane = pixel, written with tcgen05.st;
+//   B = coef (hi = the f32 row, lo = x - tf32(x)) in shared memory, MN-major
+//       SWIZZLE_128B_BASE32B (atoms of 4 entries x 32 channels);
+//   D = img in TMEM (lane = pixel, column = channel).
+// Two groups of 4 weight warps take alternate chunks; a group owns its A and
+// B stage, stages both operands of its chunk (the coef rows of the entries
+// the pass-A used mask marks -- rows of other entries keep stale finite data
+// and meet zero weights), and signals one barrier.  The coef loads are
+// issued before the alpha math so their latency hides under it.  One thread
+// issues 4 K-steps x 3 (Wh.ch + Wh.cl + Wl.ch) MMAs per chunk.
+// (A dedicated producer warp, cp.async or TMA tile::gather4, was measured
+// slower: its serial issue time per chunk set the critical path.)
+template <int NP>
+struct PxbCfg {
+  static constexpr int NA = (NP + 31) / 32;            // 32-channel atoms
+  static constexpr int PLANE = NA * 4 * 1024;          // 32 entries x NA atoms
+  static constexpr int STAGE = 2 * PLANE;              // hi | lo
+  static constexpr uint32_t D_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
+  static constexpr uint32_t A_COL0 = D_COLS;
+  static constexpr uint32_t TMEM_COLS = D_COLS + 128 <= 256 ? 256 : 512;
+  static constexpr int THREADS = 288;                  // 8 weight warps + MMA warp
+  static constexpr int MIN_CTAS = TMEM_COLS == 256 ? 2 : 1;
+  // two CTAs of 9 warps must fit the 64K-register file (ncu: 112 leaves one)
+  static constexpr int MAXREG = MIN_CTAS == 2 ? 96 : 224;
+  static constexpr int PPR = NA * 8;                   // 16 B pieces per coef row
+  static constexpr int NPF = (PX_K * PPR + 127) / 128; // pieces per group thread
+};
+
+__device__ __forceinline__ uint32_t base32b_off(int k, int j, int na) {
+  // byte offset of 16 B piece j (channels 4j..4j+3) of entry k
+  return (uint32_t)((k >> 2) * (na * 512) + (j >> 3) * 512 + (k & 3) * 128 +
+                    ((((j & 7) >> 1) ^ (k & 3)) << 5) + ((j & 1) << 4));
+}
+
+// MN-major descriptor for 32-bit data: layout SWIZZLE_128B_BASE32B (type 1,
+// the only MN-major swizzle tf32 accepts -- plain SWIZZLE_128B reads zeros,
+// see scripts/umma_probe.cu).  LBO = atom stride along N (512 B), SBO =
+// stride between 4-entry groups along K (NA * 512 B).
+__device__ __forceinline__ uint64_t umma_desc_mn_b32(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(512 >> 4) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
 
 template <int NP>
-__global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
-  constexpr uint32_t ACC_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
-  constexpr uint32_t TMEM_COLS = ACC_COLS + 128 <= 256 ? 256 : 512;
-  constexpr int B_BYTES = NP * 128;         // one operand copy (hi or lo)
-  constexpr int STAGE = 2 * B_BYTES;        // hi + lo
-  constexpr int NH = NP / 2;                // channels per stager warp
-  static_assert(NP % 8 == 0 && NP <= 256, "NP");
+__global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::MAXREG)
+    k_pxb(PxArgs A) {
+  using CF = PxbCfg<NP>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sB = sm;                                    // [2 stages][hi|lo]
-  float4* s_rec = (float4*)(sm + 2 * STAGE);                 // [8 warps][32][2]
+  unsigned char* sB = sm;  // [2 stages][hi|lo][8 entry groups][NA atoms][4 rows][128 B]
+  __shared__ __align__(16) float4 s_rec[8][2 * PX_K];  // per weight warp
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_done;
   __shared__ uint32_t s_tmem;
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const long long t_start = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CtaGeom g = cta_geom(A, blockIdx.x);
   const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
@@ -359,23 +445,22 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
   const int col0 = blockIdx.y * NP;
 
   if (threadIdx.x == 0) {
-    mbar_init(&s_full[0], 6);
-    mbar_init(&s_full[1], 6);
-    mbar_init(&s_empty[0], 1);
-    mbar_init(&s_empty[1], 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&s_full[k], 4);
+      mbar_init(&s_empty[k], 1);
+    }
     mbar_init(&s_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 10) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
-                 "r"(TMEM_COLS));
+                 "r"(CF::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
-  // operands must be finite: zero both B stages once (entries past a
-  // chunk's end then meet zero weights, never NaN garbage)
-  for (int i = threadIdx.x; i < 2 * STAGE / 16; i += blockDim.x)
-    ((float4*)sB)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  // unloaded rows keep whatever the stage held: start from zeros (finite)
+  for (int t = threadIdx.x; t < 2 * CF::STAGE / 16; t += blockDim.x)
+    ((float4*)sB)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -383,28 +468,69 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
   const uint32_t tmem = s_tmem;
 
   if (warp < 8) {
-    // ---------------- weight warps: group gq takes chunks c = gq (mod 2)
-    const int gq = warp >> 2, q = warp & 3;
+    // ---------------- weight groups: group gq takes chunks c = gq (mod 2)
+    const int gq = warp >> 2, q = warp & 3, gt = q * 32 + lane;  // thread in group
     const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
     const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
     const float teps = A.t_eps, wf = A.wf, inv_w = A.inv_w;
-    float4* rs = s_rec + warp * 64;
-    const uint32_t a_hi = tmem + ((uint32_t)(32 * q) << 16) + ACC_COLS + 64 * gq;
+    float4* rs = s_rec[warp];
+    const uint32_t a_hi = tmem + ((uint32_t)(32 * q) << 16) + CF::A_COL0 + 64 * gq;
     const uint32_t a_lo = a_hi + 32;
+    unsigned char* bhi = sB + gq * CF::STAGE;
+    unsigned char* blo = bhi + CF::PLANE;
+    const bool vec = (A.Cp & 3) == 0;
+    const int ncol = (int)min((int64_t)NP, A.Cp - col0);   // channels of this CTA
+    const int ppr = (ncol + 3) >> 2;                        // pieces with channels
+    float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
+    float nT = 0.f;
+    uint32_t nused = 0;
+    auto prefetch = [&](int c) {
+      if (c < nch) {
+        const int64_t slot = slot0 + c;
+        n0 = A.ch_rec[2 * (slot * PX_K + lane)];
+        n1 = A.ch_rec[2 * (slot * PX_K + lane) + 1];
+        nT = A.ch_T[slot * 128 + q * 32 + lane];
+        nused = A.ch_used[slot];
+      }
+    };
+    prefetch(gq);
+    long long tw = 0, tc = 0;
     for (int c = gq; c < nch; c += 2) {
       const int k = c >> 1;
-      const int64_t slot = slot0 + c;
-      const uint32_t idx = A.ch_idx[slot * PX_K + lane];
-      float T = A.ch_T[slot * 128 + q * 32 + lane];
-      float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-      if (idx != 0xffffffffu) {
-        r0 = __ldg(A.rrec + 2 * (size_t)idx);
-        r1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
-      }
+      float T = nT;
+      const uint32_t used = nused;
       __syncwarp();  // previous chunk's readers are done with rs
-      rs[2 * lane] = r0;
-      rs[2 * lane + 1] = r1;
+      rs[2 * lane] = n0;
+      rs[2 * lane + 1] = n1;
+      prefetch(c + 2);
       __syncwarp();
+      // coef rows of the used entries, issued now and consumed after the
+      // alpha math: piece p = gt + 128 u of the 32 x PPR (entry, 16 B piece)
+      // grid; entry e is uniform per warp for PPR >= 32
+      float4 cv[CF::NPF];
+#pragma unroll
+      for (int u = 0; u < CF::NPF; ++u) {
+        const int p = gt + 128 * u;
+        const int e = p / CF::PPR, jj = p - e * CF::PPR;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < PX_K && jj < ppr && ((used >> e) & 1u)) {
+          const int idx = __float_as_int(rs[2 * e + 1].w);
+          if (idx >= 0) {
+            const float* row = A.coef + (int64_t)idx * A.Cp + col0 + 4 * jj;
+            if (vec) {
+              v = __ldg((const float4*)row);
+            } else {
+              const int nv = ncol - 4 * jj;
+              v.x = __ldg(row);
+              if (nv > 1) v.y = __ldg(row + 1);
+              if (nv > 2) v.z = __ldg(row + 2);
+              if (nv > 3) v.w = __ldg(row + 3);
+            }
+          }
+        }
+        cv[u] = v;
+      }
+      const long long t0 = clock64();
       float wv[PX_K];
       if (__any_sync(0xffffffffu, T >= teps)) {
 #pragma unroll
@@ -418,90 +544,73 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
 #pragma unroll
         for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
       }
-      if (k >= 1) mbar_wait(&s_empty[gq], (k - 1) & 1);
+      const long long t1 = clock64();
+      if (k >= 1) mbar_wait_sleep(&s_empty[gq], (k - 1) & 1);
+      const long long t2 = clock64();
+      tc += t1 - t0;
+      tw += t2 - t1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float v = wv[16 * hh + j];
-          const uint32_t hb = __float_as_uint(v) & 0xFFFFE000u;
-          hi[j] = hb;
-          lo[j] = __float_as_uint(v - __uint_as_float(hb));
+        for (int jx = 0; jx < 16; ++jx) {
+          const float v = wv[16 * hh + jx];
+          hi[jx] = __float_as_uint(v) & 0xFFFFE000u;
+          lo[jx] = __float_as_uint(v - __uint_as_float(hi[jx]));
         }
         tmem_st16(a_hi + 16 * hh, hi);
         tmem_st16(a_lo + 16 * hh, lo);
       }
+      // coef hi/lo planes of the used rows (rows of unused entries untouched)
+#pragma unroll
+      for (int u = 0; u < CF::NPF; ++u) {
+        const int p = gt + 128 * u;
+        const int e = p / CF::PPR, jj = p - e * CF::PPR;
+        if (e < PX_K && jj < ppr && ((used >> e) & 1u)) {
+          const float4 x = cv[u];
+          float4 h;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          const uint32_t off = base32b_off(e, jj, CF::NA);
+          *(float4*)(bhi + off) = h;
+          *(float4*)(blo + off) = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        }
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_full[gq]);
     }
-  } else if (warp < 10) {
-    // ---------------- stagers: coef^T of the chunk -> B (K-major SW128)
-    // lane = chunk entry (row of coef), channels in blocks of SB registers
-    constexpr int SB = NH <= 64 ? NH : 32;
-    const int h0 = (warp - 8) * NH;  // first channel of this warp
-    const bool vec = (A.Cp & 3) == 0;
-    for (int c = 0; c < nch; ++c) {
-      const int s = c & 1, k = c >> 1;
-      const uint32_t idx = A.ch_idx[(slot0 + c) * PX_K + lane];
-      unsigned char* bhi = sB + s * STAGE;
-      unsigned char* blo = bhi + B_BYTES;
-#pragma unroll 1
-      for (int jb = 0; jb < NH; jb += SB) {
-        float v[SB];
-        const int64_t cb = col0 + h0 + jb;
-        const float* row = A.coef + (int64_t)idx * A.Cp + cb;
-        const int64_t rem = A.Cp - cb;
-        const int nv = rem < SB ? (int)rem : SB;
-        if (idx == 0xffffffffu || nv <= 0) {
-#pragma unroll
-          for (int j = 0; j < SB; ++j) v[j] = 0.f;
-        } else if (vec && nv == SB) {
-#pragma unroll
-          for (int j = 0; j < SB; j += 4) {
-            const float4 t = __ldg((const float4*)(row + j));
-            v[j] = t.x;
-            v[j + 1] = t.y;
-            v[j + 2] = t.z;
-            v[j + 3] = t.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < SB; ++j) v[j] = j < nv ? __ldg(row + j) : 0.f;
-        }
-        if (jb == 0 && k >= 1) mbar_wait(&s_empty[s], (k - 1) & 1);
-#pragma unroll
-        for (int j = 0; j < SB; ++j) {
-          const float hv = __uint_as_float(__float_as_uint(v[j]) & 0xFFFFE000u);
-          const uint32_t off = sw128_off(h0 + jb + j, lane);
-          *(float*)(bhi + off) = hv;
-          *(float*)(blo + off) = v[j] - hv;
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_full[s]);
+    if (A.dbg && lane == 0 && q == 0) {
+      A.dbg[blockIdx.x * 16 + 6 + gq] = tw;
+      A.dbg[blockIdx.x * 16 + 8 + gq] = tc;
     }
   } else if (lane == 0) {
-    // ---------------- MMA issuer
-    // instruction descriptor: D f32, A/B tf32, K-major, N = NP, M = 128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
+    // ---------------- MMA issuer (warp 8)
+    // instruction descriptor: D f32, A/B tf32, A K-major, B MN-major,
+    // N = NP, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
+                           ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    long long twa = 0;
     for (int c = 0; c < nch; ++c) {
-      const int s = c & 1, k = c >> 1;
-      mbar_wait(&s_full[s], k & 1);
+      const int s = c & 1;
+      const long long t0 = clock64();
+      mbar_wait(&s_full[s], (c >> 1) & 1);
+      twa += clock64() - t0;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_hi = tmem + ACC_COLS + 64 * s, a_lo = a_hi + 32;
-      const uint32_t b_hi = smem_u32(sB + s * STAGE), b_lo = b_hi + B_BYTES;
+      const uint32_t a_hi = tmem + CF::A_COL0 + 64 * s, a_lo = a_hi + 32;
+      const uint32_t b_hi = smem_u32(sB + s * CF::STAGE), b_lo = b_hi + CF::PLANE;
 #pragma unroll
       for (int ks = 0; ks < PX_K / 8; ++ks) {
         const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
-        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_sw128(b_hi + 32 * ks), idesc, acc0);
-        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_sw128(b_lo + 32 * ks), idesc, 1u);
-        mma_tf32_ts(tmem, a_lo + 8 * ks, umma_desc_sw128(b_hi + 32 * ks), idesc, 1u);
+        const uint32_t ko = ks * CF::NA * 1024;  // 8 entries = 2 atom rows of K
+        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_mn_b32(b_hi + ko, CF::NA * 512), idesc, acc0);
+        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_mn_b32(b_lo + ko, CF::NA * 512), idesc, 1u);
+        mma_tf32_ts(tmem, a_lo + 8 * ks, umma_desc_mn_b32(b_hi + ko, CF::NA * 512), idesc, 1u);
       }
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -512,6 +621,7 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&s_done))
         : "memory");
+    if (A.dbg) A.dbg[blockIdx.x * 16 + 0] = twa;
   }
 
   // ---------------- epilogue: warps 0..3 own TMEM lanes 32q.. (= pixels)
@@ -520,7 +630,7 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
     const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
     const bool inside = px < A.w && py < A.h;
     if (nch > 0) {
-      mbar_wait(&s_done, 0);
+      mbar_wait_sleep(&s_done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
@@ -537,7 +647,7 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0u;
+        for (int jx = 0; jx < 8; ++jx) v[jx] = 0u;
       }
       const int64_t cc0 = col0 + c0;
       if (!inside || cc0 >= A.Cp) continue;
@@ -550,11 +660,11 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
                              __uint_as_float(v[7]));
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int64_t cc = cc0 + j;
+        for (int jx = 0; jx < 8; ++jx) {
+          const int64_t cc = cc0 + jx;
           if (cc < A.Cp) {
             const int64_t b = cc / A.C, ch = cc - b * A.C;
-            A.img[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch] = __uint_as_float(v[j]);
+            A.img[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch] = __uint_as_float(v[jx]);
           }
         }
       }
@@ -562,24 +672,41 @@ __global__ void __launch_bounds__(PXB_THREADS, 2) k_pxb(PxArgs A) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 10) {
+  if (warp == 8) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+                 "r"(CF::TMEM_COLS));
+  }
+  if (A.dbg && threadIdx.x == 0) {
+    A.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
+    A.dbg[blockIdx.x * 16 + 11] = nch;
   }
 }
 
+long long* gsparc_dbg_ptr = nullptr;  // experiments: last pass-B timing buffer
+
 template <int NP>
 static void launch_pxb(const PxArgs& A, int chunks_y, cudaStream_t st) {
-  constexpr int STAGE = 2 * NP * 128;
-  // >= 80 KB keeps residency at two CTAs per SM (the TMEM budget)
-  size_t smem = 2 * STAGE + 8 * 64 * 16 + 1024;
-  if (smem < 80 * 1024) smem = 80 * 1024;
+  using CF = PxbCfg<NP>;
+  size_t smem = 2 * CF::STAGE + 1024;
+  // two CTAs per SM at most (TMEM); keep a third from being scheduled
+  if (CF::MIN_CTAS == 2 && smem < 78 * 1024) smem = 78 * 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_pxb<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // without this the driver picks a ~100 KB carveout: one CTA per SM
+    cudaFuncSetAttribute(k_pxb<NP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     attr = true;
   }
-  k_pxb<NP><<<dim3(A.ntiles * 2, chunks_y), PXB_THREADS, smem, st>>>(A);
+  PxArgs B = A;
+  static long long* dbg = nullptr;
+  if (getenv("GSPARC_PXB_DBG")) {  // experiments only
+    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * 4096);
+    cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * 4096, st);
+    B.dbg = dbg;
+    gsparc_dbg_ptr = dbg;
+  }
+  k_pxb<NP><<<dim3(A.ntiles * 2, chunks_y), CF::THREADS, smem, st>>>(B);
 }
 
 static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
@@ -589,7 +716,10 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.tile_start = (const int*)(frame + L.off_tile_start);
   A.rrec = (const float4*)(frame + L.off_rrec);
   A.coef = (const float*)(frame + L.off_coef);
+  A.ch_used = (uint32_t*)(frame + L.off_ch_used);
+  A.dbg = nullptr;
   A.ch_idx = (uint32_t*)(frame + L.off_ch_idx);
+  A.ch_rec = (float4*)(frame + L.off_ch_rec);
   A.ch_T = (float*)(frame + L.off_ch_T);
   A.ch_n = (int*)(frame + L.off_ch_n);
   A.wstop = (int*)(frame + L.off_wstop);
@@ -601,6 +731,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.counters = (int*)(frame + L.off_counters);
   A.img = (float*)img;
   A.Cp = (int64_t)n_tx * C;
+  A.n = L.n;
   A.C = C;
   A.w = L.width;
   A.h = L.height;
