@@ -177,14 +177,19 @@ __device__ void bitonic_sort(uint64_t* a, int n) {
   }
 }
 
-// Re-order runs that tie on the coarse 32-bit depth by the full f64 key.
-__device__ void fix_coarse_ties(uint64_t* a, int n, const uint64_t* key) {
+// Re-order runs that tie on the sort key (coarse depth, reduced by `shift`
+// relative to `cmin`) by the full f64 key, then the source index.
+__device__ __forceinline__ uint32_t sort_digits(uint64_t v, uint32_t cmin, int shift) {
+  return ((uint32_t)(v >> 32) - cmin) >> shift;
+}
+__device__ void fix_coarse_ties(uint64_t* a, int n, const uint64_t* key, uint32_t cmin = 0,
+                                int shift = 0) {
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    uint32_t cj = (uint32_t)(a[j] >> 32);
-    bool head = (j == 0) || ((uint32_t)(a[j - 1] >> 32) != cj);
-    if (!head || j + 1 >= n || (uint32_t)(a[j + 1] >> 32) != cj) continue;
+    uint32_t cj = sort_digits(a[j], cmin, shift);
+    bool head = (j == 0) || (sort_digits(a[j - 1], cmin, shift) != cj);
+    if (!head || j + 1 >= n || sort_digits(a[j + 1], cmin, shift) != cj) continue;
     int e = j + 1;
-    while (e < n && (uint32_t)(a[e] >> 32) == cj) ++e;
+    while (e < n && sort_digits(a[e], cmin, shift) == cj) ++e;
     // insertion sort a[j..e) by (key64[idx], idx)
     for (int p = j + 1; p < e; ++p) {
       uint64_t v = a[p];
@@ -280,25 +285,23 @@ __device__ void reg_bitonic(uint64_t (&x)[RB_E], uint64_t* sm, int np2) {
 }
 
 // Block LSD radix sort of one tile's packed keys (coarse_depth32 << 32 |
-// index) in shared memory: 8-bit digits over the index bits actually used and
-// the 32 coarse-depth bits.  Keys are ranked warp by warp in list order
-// (warp-striped: key i = 256 w + 32 e + lane) with ballot-derived peers, so
-// every pass is stable and the result is the exact u64 order.  Cost O(n) per
-// pass, against O(n log^2 n) for the bitonic network it replaces.
+// index) in shared memory on the tile-relative key
+//     d = (coarse - cmin) >> shift   (at most 24 significant bits)
+// in 8-bit digits, only as many passes as d has bytes.  Elements are ranked
+// warp by warp in list order (warp-striped: key i = 256 w + 32 e + lane) with
+// __match_any_sync peers, so every pass is stable; elements that tie on d are
+// put in exact (full key, index) order by fix_coarse_ties afterwards.
 constexpr int RS_T = 1024;
 constexpr int RS_W = RS_T / 32;
 constexpr int RS_E = 8;
 constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
 
-__device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, int idx_bits) {
+__device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n,
+                                      uint32_t cmin, int shift, int npass) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  int shifts[8];
-  int np = 0;
-  for (int b = 0; b < idx_bits; b += 8) shifts[np++] = b;
-  for (int b = 32; b < 64; b += 8) shifts[np++] = b;
-  for (int pass = 0; pass < np; ++pass) {
-    const int sh = shifts[pass];
+  for (int pass = 0; pass < npass; ++pass) {
+    const int sh = 8 * pass;
     int* wc = cnt + warp * 256;
     for (int d = lane; d < 256; d += 32) wc[d] = 0;
     __syncwarp();
@@ -309,15 +312,8 @@ __device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, 
     for (int e = 0; e < RS_E; ++e) {
       const int i = wbase + e * 32 + lane;
       const bool valid = i < n;
-      const int d = valid ? (int)((src[valid ? i : 0] >> sh) & 0xFF) : 0;
-      // peers with the same 8-bit digit: AND of 8 bit-plane ballots
-      unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const unsigned m = __ballot_sync(0xffffffffu, (d >> b) & 1);
-        peers &= ((d >> b) & 1) ? m : ~m;
-      }
-      if (!valid) peers = 1u << lane;
+      const int d = valid ? (int)((sort_digits(src[valid ? i : 0], cmin, shift) >> sh) & 0xFF) : 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x1000 + lane);
       const int leader = __ffs(peers) - 1;
       int old = 0;
       if (valid && lane == leader) {
@@ -327,6 +323,7 @@ __device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, 
       old = __shfl_sync(0xffffffffu, old, leader);
       rank[e] = old + __popc(peers & lt);
       dig[e] = d;
+      __syncwarp();
     }
     __syncthreads();
     // offsets: digit-major, warp-minor
@@ -372,11 +369,7 @@ __device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, 
     src = dst;
     dst = t;
   }
-  // result is in `src` after the loop swap; copy back if needed
-  if (np & 1) {
-    for (int i = tid; i < n; i += blockDim.x) dst[i] = src[i];
-    __syncthreads();
-  }
+  return src;  // buffer holding the result
 }
 
 // Sort each tile's bucket by (coarse depth, index), fix coarse ties by the
@@ -385,7 +378,7 @@ __device__ void block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n, 
 __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* tile_start,
                                                     const uint64_t* key, int* counters,
                                                     const float4* rec32, float4* pair_rec,
-                                                    int idx_bits) {
+                                                    int /*unused*/) {
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
   if (counters[GSPARC_CNT_OVERFLOW]) return;
   const int t = blockIdx.x;
@@ -395,12 +388,35 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* 
     uint64_t* a = s_keys;
     uint64_t* b = s_keys + RS_CAP;
     int* cnt = (int*)(s_keys + 2 * RS_CAP);
-    for (int j = threadIdx.x; j < n; j += blockDim.x) a[j] = g[j];
+    __shared__ uint32_t s_mm[2];
+    if (threadIdx.x == 0) {
+      s_mm[0] = 0xFFFFFFFFu;
+      s_mm[1] = 0u;
+    }
     __syncthreads();
-    block_radix_sort(a, b, cnt, n, idx_bits);
-    fix_coarse_ties(a, n, key);
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint64_t v = g[j];
+      a[j] = v;
+      const uint32_t c = (uint32_t)(v >> 32);
+      lo = min(lo, c);
+      hi = max(hi, c);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_mm[0], lo);
+      atomicMax(&s_mm[1], hi);
+    }
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = a[j];
+    const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
+    const int bits = span ? 32 - __clz(span) : 0;
+    const int shift = bits > 24 ? bits - 24 : 0;
+    const int npass = (bits - shift + 7) / 8;  // 0..3
+    uint64_t* r = block_radix_sort(a, b, cnt, n, cmin, shift, npass);
+    fix_coarse_ties(r, n, key, cmin, shift);
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = r[j];
   } else if (n > RS_CAP) {
     if (threadIdx.x == 0) atomicAdd(counters + GSPARC_CNT_BIGTILE, 1);
     bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
