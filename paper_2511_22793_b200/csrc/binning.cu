@@ -308,21 +308,28 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
     int rank[RS_E];
     int dig[RS_E];
     const int wbase = warp * 32 * RS_E;
+    // all peer masks first (independent MATCH latencies overlap), then the
+    // per-warp digit counters in element order (stable)
+    unsigned peers[RS_E];
 #pragma unroll
     for (int e = 0; e < RS_E; ++e) {
       const int i = wbase + e * 32 + lane;
       const bool valid = i < n;
       const int d = valid ? (int)((sort_digits(src[valid ? i : 0], cmin, shift) >> sh) & 0xFF) : 0;
-      const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0x1000 + lane);
-      const int leader = __ffs(peers) - 1;
+      peers[e] = __match_any_sync(0xffffffffu, valid ? d : 0x1000 + lane);
+      dig[e] = valid ? d : -1;
+    }
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int d = dig[e];
+      const int leader = __ffs(peers[e]) - 1;
       int old = 0;
-      if (valid && lane == leader) {
+      if (d >= 0 && lane == leader) {
         old = wc[d];
-        wc[d] = old + __popc(peers);
+        wc[d] = old + __popc(peers[e]);
       }
       old = __shfl_sync(0xffffffffu, old, leader);
-      rank[e] = old + __popc(peers & lt);
-      dig[e] = d;
+      rank[e] = old + __popc(peers[e] & lt);
       __syncwarp();
     }
     __syncthreads();

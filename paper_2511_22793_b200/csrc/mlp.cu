@@ -24,8 +24,7 @@ struct MlpArgs {
   const float4* rec32;
   const double* rec64;
   const uint64_t* key;
-  const int* live;       // live flags (K4 pass A); nullptr -> all kept
-  int* counters_rw;      // CNT_LIVE is counted here when `live` is set
+  const int* live_list;  // live Gaussians (K4 pass A); nullptr -> all kept
   const int* counters;
   void* coef;
   int64_t n;
@@ -44,16 +43,10 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gi = t / A.B;
   const int b = (int)(t % A.B);
-  if (gi >= A.n) return;
-  const int64_t i = gi;
-  if (A.live) {
-    const bool lv = A.live[i] != 0;
-    const unsigned m = __ballot_sync(__activemask(), lv && b == 0);
-    if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(A.counters_rw + GSPARC_CNT_LIVE, __popc(m));
-    if (!lv) return;
-  } else if (A.key[i] == ~0ULL) {
-    return;
-  }
+  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  if (gi >= count) return;
+  const int64_t i = A.live_list ? A.live_list[gi] : gi;
+  if (!A.live_list && A.key[i] == ~0ULL) return;
   R theta, phi;
   if constexpr (sizeof(R) == 4) {
     float4 r = A.rec32[2 * i + 1];
@@ -147,7 +140,10 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
     const float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
     const float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
     const float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
-    const double d = tx_distance(p, txb);
+    // s / d_tx (rasterizer.py:200): one f64 reciprocal per (Gaussian, TX);
+    // x * (1/d) differs from x / d by <= 1 ulp in f64, invisible after the
+    // cast to f32 except on exact rounding ties
+    const double rd = 1.0 / tx_distance(p, txb);
     float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
 #pragma unroll
     for (int u = 0; u < MAXV; ++u) {
@@ -156,40 +152,18 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
       float part = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
       part += __shfl_xor_sync(0xffffffffu, part, 1);
       part += __shfl_xor_sync(0xffffffffu, part, 2);
-      if (q == 0 && f < nvec) out[f >> 2] = (float)((double)(part + bv[u]) / d);
+      if (q == 0 && f < nvec) out[f >> 2] = (float)((double)(part + bv[u]) * rd);
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_mlp_wide(MlpArgs A) {
+__global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (A.live) {
-    // CTA-level compaction of 256 live flags, then warps take the live
-    // Gaussians round robin (balances the Poisson spread of live flags)
-    __shared__ int s_list[256];
-    __shared__ int s_wc[8], s_n;
-    const int warp = threadIdx.x >> 5;
-    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    const bool lv = j < A.n && A.live[j] != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, lv);
-    if (lane == 0) s_wc[warp] = __popc(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int run = 0;
-      for (int k = 0; k < 8; ++k) {
-        const int c = s_wc[k];
-        s_wc[k] = run;
-        run += c;
-      }
-      s_n = run;
-      if (run) atomicAdd(A.counters_rw + GSPARC_CNT_LIVE, run);
-    }
-    __syncthreads();
-    if (lv) s_list[s_wc[warp] + __popc(m & ((1u << lane) - 1u))] = (int)j;
-    __syncthreads();
-    for (int k = warp; k < s_n; k += 8) mlp_wide_one(A, s_list[k], lane);
+  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  if (A.live_list) {  // one warp per live Gaussian, all in flight
+    for (int64_t gi = wid; gi < count; gi += nwarps) mlp_wide_one(A, A.live_list[gi], lane);
     return;
   }
   for (int64_t gi = wid; gi < A.n; gi += nwarps) {
@@ -208,8 +182,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
   A.rec32 = (const float4*)(frame + L.off_rec32);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.key = (const uint64_t*)(frame + L.off_key);
-  A.live = live_only ? (const int*)(frame + L.off_live) : nullptr;
-  A.counters_rw = (int*)(frame + L.off_counters);
+  A.live_list = live_only ? (const int*)(frame + L.off_live_list) : nullptr;
   A.counters = (const int*)(frame + L.off_counters);
   A.coef = frame + L.off_coef;
   A.n = cloud.n;
@@ -240,7 +213,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
   } else if (A.C % 4 == 0 && A.C >= 16 && A.C <= 128 && A.H == 16 && A.I == 5) {
     int64_t threads = cloud.n * 32;
     int64_t blocks = (threads + 255) / 256;
-    if (live_only) blocks = (cloud.n + 255) / 256;  // a CTA per 256 live flags
+    if (live_only && blocks > 148 * 16) blocks = 148 * 16;  // grid-stride over the list
     k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
   } else {
     int64_t threads = cloud.n * B;

@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(256) k_raster(RasterArgs A) {
       for (int e = tid; e < nch; e += blockDim.x) {
         if (s_live[e]) {
           const int idx = s_idx[e];
-          A.live[idx] = 1;  // flags; the MLP compacts and counts them
+          if (A.live[idx] == 0 && atomicExch(A.live + idx, 1) == 0) {
+            const int pos = atomicAdd(A.counters + GSPARC_CNT_LIVE, 1);
+            A.live_list[pos] = idx;
+          }
         }
       }
     }

@@ -313,8 +313,6 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         if (um) {
           lastch = c + 1;
           if (lane == 0) atomicOr(A.ch_used + slot0 + c, um);
-          // fire-and-forget flag; the MLP compacts the flags itself
-          if ((um >> lane) & 1u) A.live[__float_as_int(s_ring[s][lane][1].w)] = 1;
         }
         wdone = !__any_sync(0xffffffffu, T >= teps);
         if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
@@ -343,6 +341,18 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   }
   __syncthreads();
   if (threadIdx.x == 0) A.ch_n[blockIdx.x] = s_nch;
+  // live list (for the lazy MLP): entries of this CTA's chunks with an
+  // included contribution; the first CTA to flag a Gaussian appends it.
+  // Done once per CTA, off the per-chunk critical path.
+  const int nused = s_nch * PX_K;
+  for (int t = threadIdx.x; t < nused; t += blockDim.x) {
+    const int c = t >> 5, e = t & 31;
+    const uint32_t used = __ldcg(A.ch_used + slot0 + c);
+    if ((used >> e) & 1u) {
+      const int idx = (int)__ldcg(A.ch_idx + (slot0 + c) * PX_K + e);
+      if (atomicExch(A.live + idx, 1) == 0) A.live_list[atomicAdd(A.counters + GSPARC_CNT_LIVE, 1)] = idx;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ pass B
