@@ -132,6 +132,11 @@ typedef struct gsparc_frame_layout {
   int64_t ch_slots;       /* chunk slots (>= 2*(pairs+31*ntiles)/32 + 2) */
   int64_t off_ch_used;    /* u32  [slots] entries of a chunk with at least
                              one included contribution in the CTA        */
+  int64_t off_det_gcoef;  /* dtype [pair_capacity,4,channels] per (list
+                             entry, sub-tile) dL/dcoef partials
+                             (with_backward == 2: deterministic backward) */
+  int64_t off_det_ggeo;   /* dtype [pair_capacity,4,max(1,ceil(ch/4)),6]
+                             geometric partials (with_backward == 2)      */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);
@@ -178,7 +183,8 @@ int gsparc_render_forward(const gsparc_cloud* cloud, const gsparc_view* view,
  * written (overwritten) into grad_flat = positions|log_scales|rotations|
  * raw_opacities|mlp_weights, n*(11+P) floats of `grad_dtype`.
  * dL_dev: frame dtype [n_tx, h, w, C].  Requires the matching forward's
- * frame (fused pass, same tx). deterministic: fixed-order reduction. */
+ * frame (fused pass, same tx). deterministic: fixed-order reduction (bit-identical reruns); needs a frame
+ * planned with with_backward == 2. */
 int gsparc_render_backward(const gsparc_cloud* cloud, const gsparc_view* view,
                            const double* tx_dev, int32_t n_tx,
                            const void* dL_dev, int32_t deterministic,

@@ -50,7 +50,8 @@ class CLayout(ctypes.Structure):
                 [(k, c_i32) for k in ("width", "height", "ntx", "nty", "ntiles",
                                       "dtype", "with_backward", "reserved")] +
                 [("off_" + k, c_i64) for k in _LAYOUT_OFFSETS] +
-                [("ch_slots", c_i64), ("off_ch_used", c_i64)])
+                [("ch_slots", c_i64), ("off_ch_used", c_i64),
+                 ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64)])
 
 
 class CAdamConfig(ctypes.Structure):

@@ -167,6 +167,10 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_ch_n = take(sizeof(int) * 2 * L.ntiles);
   L.off_ch_rec = take(dtype == GSPARC_F32 ? 32 * 32 * L.ch_slots : 0);
   L.off_ch_used = take(dtype == GSPARC_F32 ? 4 * L.ch_slots : 0);
+  const bool det = with_backward == 2;
+  const int64_t det_chunks = channels >= 4 ? (channels + 3) / 4 : 1;
+  L.off_det_gcoef = det ? take(esz * pair_capacity * 4 * channels) : 0;
+  L.off_det_ggeo = det ? take(esz * pair_capacity * 4 * det_chunks * 6) : 0;
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;
@@ -251,13 +255,13 @@ int gsparc_render_backward(const gsparc_cloud* cloud, const gsparc_view* view,
     set_error("render_backward: invalid arguments (frame needs with_backward)");
     return GSPARC_ERR_ARG;
   }
-  if (deterministic) {
-    set_error("render_backward: deterministic reduction not built in this version");
-    return GSPARC_ERR_UNSUPPORTED;
+  if (deterministic && L->with_backward != 2) {
+    set_error("render_backward: deterministic mode needs a frame planned with with_backward=2");
+    return GSPARC_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
   char* f = (char*)frame;
-  GS_TRY(launch_raster_backward(*L, f, n_tx, cloud->mlp_out, dL_dev, st));
+  GS_TRY(launch_raster_backward(*L, f, n_tx, cloud->mlp_out, dL_dev, deterministic != 0, st));
   return launch_gauss_backward(*cloud, *view, tx_dev, n_tx, *L, f, grad_flat, grad_dtype, st);
 }
 

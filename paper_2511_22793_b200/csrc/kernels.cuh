@@ -17,7 +17,7 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
 int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C, double t_eps,
                      int pass, void* img, cudaStream_t st);
 int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
-                           const void* dL, cudaStream_t st);
+                           const void* dL, bool deterministic, cudaStream_t st);
 int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, const double* tx,
                           int B, const gsparc_frame_layout& L, char* frame, void* grad,
                           int grad_dtype, cudaStream_t st);

@@ -33,22 +33,24 @@ struct BwdArgs {
   const int* last;
   void* gcoef;  // [n, Cp]
   void* ggeo;   // [n, 8]
+  void* dgc;    // deterministic: [pairs, nsub, Cp] partials
+  void* dgg;    // deterministic: [pairs, nsub, nchunks, 6] partials
   const int* counters;
   int64_t Cp;
-  int C;
+  int C, nchunks;
   int w, h, ntx, sr, nsub;
 };
 
-template <typename R, int CB, int NB>
+template <typename R, int CB, int NB, bool DET>
 __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int P = blockDim.x;              // pixels of this sub-tile
   R* s_u = (R*)smraw;                    // [CB][P]
   R* s_wgt = s_u + CB * P;               // [NB][P]
   R* s_coef = s_wgt + NB * P;            // [NB][CB]
-  R* s_red = s_coef + NB * CB;           // [NB][6]
-  Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6);  // [NB]
-  int* s_idx = (int*)(s_rec + NB);       // [NB]
+  R* s_red = s_coef + NB * CB;           // [NB][6] (DET: [NB][8 warps][6])
+  Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6 * (DET ? 8 : 1));  // [NB]
+  int* s_idx = (int*)(s_rec + NB);       // [NB]; bit 31: first copy of a seam duplicate
   float4* s_fr = (float4*)(((uintptr_t)(s_idx + NB) + 15) & ~(uintptr_t)15);  // [NB][2] (f32)
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   const int px = tx_ * TILE + (pix & (TILE - 1));
   const int py = ty * TILE + part * A.sr + pix / TILE;
   const bool inside = px < A.w && py < A.h;
-  const int start = A.tile_start[tile];
+  const int start = A.tile_start[tile], tile_end = A.tile_start[tile + 1];
   const int nvisit = max(A.wstop[tile * 8 + part * 2], A.wstop[tile * 8 + part * 2 + 1]);
   if (nvisit == 0) return;
   const int chunk_base = chunk * CB;
@@ -96,7 +98,13 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
     __syncthreads();
     if (tid < nb) {
       const uint32_t idx = (uint32_t)A.pairs[start + b0 + tid];
-      s_idx[tid] = (int)idx;
+      // the reference accumulates per tile with g[rows] += ... (fancy
+      // indexing, rasterizer.py:302-326): for a Gaussian listed twice in a
+      // tile (seam duplicate) only the later copy's row survives -- drop the
+      // first copy's contributions the same way
+      const int kn = start + b0 + tid + 1;
+      const bool first_dup = kn < tile_end && (uint32_t)A.pairs[kn] == idx;
+      s_idx[tid] = (int)idx | (first_dup ? (int)0x80000000 : 0);
       if constexpr (sizeof(R) == 4) {
         // conic recovered from the pre-scaled exponent coefficients
         const float4 f0 = __ldg(A.rrec + 2 * (size_t)idx), f1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       const int64_t cc = chunk_base + c;
       s_coef[e] = cc < A.Cp ? coef[(int64_t)idx * A.Cp + cc] : R(0);
     }
-    for (int e = tid; e < nb * 6; e += blockDim.x) s_red[e] = R(0);
+    for (int e = tid; e < nb * 6 * (DET ? 8 : 1); e += blockDim.x) s_red[e] = R(0);
     __syncthreads();
     for (int j = nb - 1; j >= 0; --j) {
       const int k = b0 + j;
@@ -162,13 +170,23 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
         gm0 = warp_sum(gm0);
         gm1 = warp_sum(gm1);
         if (lane == 0) {
-          R* rr = s_red + j * 6;
-          atomicAdd(rr + 0, gc0);
-          atomicAdd(rr + 1, gc1);
-          atomicAdd(rr + 2, gc2);
-          atomicAdd(rr + 3, gm0);
-          atomicAdd(rr + 4, gm1);
-          atomicAdd(rr + 5, g_sig);
+          if constexpr (DET) {  // one slot per warp, summed in warp order
+            R* rr = s_red + (j * 8 + (tid >> 5)) * 6;
+            rr[0] = gc0;
+            rr[1] = gc1;
+            rr[2] = gc2;
+            rr[3] = gm0;
+            rr[4] = gm1;
+            rr[5] = g_sig;
+          } else {
+            R* rr = s_red + j * 6;
+            atomicAdd(rr + 0, gc0);
+            atomicAdd(rr + 1, gc1);
+            atomicAdd(rr + 2, gc2);
+            atomicAdd(rr + 3, gm0);
+            atomicAdd(rr + 4, gm1);
+            atomicAdd(rr + 5, g_sig);
+          }
         }
       }
     }
@@ -183,23 +201,42 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       R s = R(0);
 #pragma unroll 8
       for (int q = 0; q < P; ++q) s += wr[q] * ur[q];
-      if (s != R(0)) atomicAdd(gcoef + (int64_t)s_idx[j] * A.Cp + cc, s);
+      const int sj = s_idx[j];
+      if (sj < 0) s = R(0);  // first copy of a seam duplicate
+      if constexpr (DET) {
+        const int64_t k = start + b0 + j;  // list position
+        ((R*)A.dgc)[(k * A.nsub + part) * A.Cp + cc] = s;
+      } else {
+        if (s != R(0)) atomicAdd(gcoef + (int64_t)sj * A.Cp + cc, s);
+      }
     }
     for (int o = tid; o < nb * 6; o += blockDim.x) {
-      const R v = s_red[o];
-      if (v != R(0)) atomicAdd(ggeo + (int64_t)s_idx[o / 6] * 8 + (o % 6), v);
+      if constexpr (DET) {
+        const int j = o / 6, f = o % 6;
+        const int nw = P >> 5;
+        R v = R(0);
+        for (int w = 0; w < nw; ++w) v += s_red[(j * 8 + w) * 6 + f];
+        if (s_idx[j] < 0) v = R(0);  // first copy of a seam duplicate
+        const int64_t k = start + b0 + j;
+        ((R*)A.dgg)[((k * A.nsub + part) * A.nchunks + chunk) * 6 + f] = v;
+      } else {
+        const R v = s_red[o];
+        const int sj = s_idx[o / 6];
+        if (v != R(0) && sj >= 0) atomicAdd(ggeo + (int64_t)sj * 8 + (o % 6), v);
+      }
     }
   }
 }
 
-template <typename R, int CB, int NB>
+template <typename R, int CB, int NB, bool DET>
 static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   const int P = TILE * A.sr;
-  const size_t smem_max = sizeof(R) * ((size_t)CB * 256 + (size_t)NB * 256 + NB * CB + NB * 6) +
+  constexpr size_t RED = NB * 6 * (DET ? 8 : 1);
+  const size_t smem_max = sizeof(R) * ((size_t)CB * 256 + (size_t)NB * 256 + NB * CB + RED) +
                           sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
-  const size_t smem = sizeof(R) * ((size_t)CB * P + (size_t)NB * P + NB * CB + NB * 6) +
+  const size_t smem = sizeof(R) * ((size_t)CB * P + (size_t)NB * P + NB * CB + RED) +
                       sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
-  auto kern = k_raster_bwd<R, CB, NB>;
+  auto kern = k_raster_bwd<R, CB, NB, DET>;
   static bool attr_set = false;  // one per instantiation; keeps capture clean
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
@@ -210,8 +247,110 @@ static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   return check_launch("k_raster_bwd");
 }
 
+// Deterministic mode, step 2: per Gaussian (one warp), sum the partials of
+// every list entry it owns in a fixed order -- tiles in (ty, tx) order over
+// the a segment then the b-only tiles (rasterizer.py:117-141), the seam
+// duplicate right after its first copy, then sub-tiles, then channel chunks.
+// An entry's list position is found by binary search on (f64 key, index),
+// the order the tile lists are sorted in.
+struct RedArgs {
+  const uint64_t* pairs;
+  const int* tile_start;
+  const int* wstop;
+  const uint64_t* key;
+  const int4* rect;
+  const void* dgc;
+  const void* dgg;
+  void* gcoef;
+  void* ggeo;
+  int64_t n, Cp;
+  int nchunks, ntx, nsub;
+};
+
+constexpr int RED_MAXT = 320;  // tiles per Gaussian (2 x 138 at 90x360 + seam)
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
+  __shared__ int s_pos[8][RED_MAXT];   // list position per enumerated tile
+  __shared__ short s_tile[8][RED_MAXT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 8 + warp;
+  if (i >= A.n) return;
+  R* gc = (R*)A.gcoef + i * A.Cp;
+  R* gg = (R*)A.ggeo + i * 8;
+  const uint64_t ki = A.key[i];
+  int ntile = 0, na = 0, nbo = 0, rows = 0, y0 = 0, a0 = 0, b1 = -1;
+  if (ki != ~0ULL) {
+    const int4 r = A.rect[i];
+    y0 = r.x & 0xffff;
+    const int y1 = r.x >> 16;
+    a0 = r.y & 0xffff;
+    const int a1 = r.y >> 16;
+    b1 = r.z >> 16;  // b segment is [0, b1] (wrapped), empty if b1 < 0
+    na = a1 - a0 + 1;
+    nbo = b1 >= 0 ? min(b1, a0 - 1) + 1 : 0;  // b tiles outside the a range
+    rows = y1 - y0 + 1;
+    ntile = rows * (na + nbo);
+  }
+  if (ntile > RED_MAXT) ntile = RED_MAXT;  // cannot happen for w <= 4096
+  for (int j = lane; j < ntile; j += 32) {
+    const int ty = y0 + j / (na + nbo), rj = j % (na + nbo);
+    const int tx = rj < na ? a0 + rj : rj - na;
+    const int t = ty * A.ntx + tx;
+    int lo = A.tile_start[t], hi = A.tile_start[t + 1];
+    while (lo < hi) {  // first entry not below (ki, i)
+      const int mid = (lo + hi) >> 1;
+      const uint32_t pi = (uint32_t)A.pairs[mid];
+      const uint64_t pk = A.key[pi];
+      if (pk < ki || (pk == ki && pi < (uint32_t)i)) lo = mid + 1;
+      else hi = mid;
+    }
+    const bool twice = rj < na && b1 >= 0 && tx <= b1;  // seam duplicate
+    s_pos[warp][j] = lo | (twice ? (1 << 30) : 0);
+    s_tile[warp][j] = (short)t;
+  }
+  __syncwarp();
+  auto visible = [&](int t, int k, int p) {
+    const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
+    return k - A.tile_start[t] < nv;
+  };
+  const R* dgc = (const R*)A.dgc;
+  const R* dgg = (const R*)A.dgg;
+  for (int64_t c0 = 0; c0 < A.Cp; c0 += 32) {
+    const int64_t cc = c0 + lane;
+    R acc = R(0);
+    if (cc < A.Cp) {
+      for (int j = 0; j < ntile; ++j) {
+        const int pv = s_pos[warp][j], t = s_tile[warp][j];
+        for (int copy = 0; copy <= (pv >> 30); ++copy) {
+          const int k = (pv & ((1 << 30) - 1)) + copy;
+          for (int p = 0; p < A.nsub; ++p)
+            if (visible(t, k, p)) acc += dgc[((int64_t)k * A.nsub + p) * A.Cp + cc];
+        }
+      }
+      gc[cc] = acc;
+    }
+  }
+  if (lane < 8) {
+    R acc = R(0);
+    if (lane < 6) {
+      for (int j = 0; j < ntile; ++j) {
+        const int pv = s_pos[warp][j], t = s_tile[warp][j];
+        for (int copy = 0; copy <= (pv >> 30); ++copy) {
+          const int k = (pv & ((1 << 30) - 1)) + copy;
+          for (int p = 0; p < A.nsub; ++p)
+            if (visible(t, k, p))
+              for (int ch = 0; ch < A.nchunks; ++ch)
+                acc += dgg[(((int64_t)k * A.nsub + p) * A.nchunks + ch) * 6 + lane];
+        }
+      }
+    }
+    gg[lane] = acc;
+  }
+}
+
 int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
-                           const void* dL, cudaStream_t st) {
+                           const void* dL, bool det, cudaStream_t st) {
   BwdArgs A;
   A.pairs = (const uint64_t*)(frame + L.off_pairs);
   A.tile_start = (const int*)(frame + L.off_tile_start);
@@ -225,6 +364,8 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.last = (const int*)(frame + L.off_last);
   A.gcoef = frame + L.off_gcoef;
   A.ggeo = frame + L.off_ggeo;
+  A.dgc = frame + L.off_det_gcoef;
+  A.dgg = frame + L.off_det_ggeo;
   A.counters = (const int*)(frame + L.off_counters);
   A.Cp = (int64_t)n_tx * C;
   A.C = C;
@@ -234,14 +375,56 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.sr = forward_sub_rows(L, A.Cp);
   A.nsub = TILE / A.sr;
   const size_t esz = L.dtype == GSPARC_F64 ? 8 : 4;
-  if (cudaMemsetAsync(A.gcoef, 0, esz * (size_t)L.n * (size_t)L.channels, st) != cudaSuccess ||
-      cudaMemsetAsync(A.ggeo, 0, esz * (size_t)L.n * 8, st) != cudaSuccess)
+  const int CB = L.dtype == GSPARC_F64 ? 4 : A.Cp <= 2 ? 2 : A.Cp <= 8 ? 8 : A.Cp <= 16 ? 16 : 32;
+  A.nchunks = (int)((A.Cp + CB - 1) / CB);
+  if (det) {
+    if (A.nsub > 4 || A.nchunks > (L.channels >= 4 ? (L.channels + 3) / 4 : 1)) {
+      set_error("raster_backward: deterministic partial buffers too small");
+      return GSPARC_ERR_UNSUPPORTED;
+    }
+  } else if (cudaMemsetAsync(A.gcoef, 0, esz * (size_t)L.n * (size_t)L.channels, st) !=
+                 cudaSuccess ||
+             cudaMemsetAsync(A.ggeo, 0, esz * (size_t)L.n * 8, st) != cudaSuccess) {
     return check_launch("bwd memset");
-  if (L.dtype == GSPARC_F64) return launch_bwd_cfg<double, 4, 32>(A, L.ntiles, st);
-  if (A.Cp <= 2) return launch_bwd_cfg<float, 2, 32>(A, L.ntiles, st);
-  if (A.Cp <= 8) return launch_bwd_cfg<float, 8, 32>(A, L.ntiles, st);
-  if (A.Cp <= 16) return launch_bwd_cfg<float, 16, 32>(A, L.ntiles, st);
-  return launch_bwd_cfg<float, 32, 32>(A, L.ntiles, st);
+  }
+  int rc;
+  if (L.dtype == GSPARC_F64) {
+    rc = det ? launch_bwd_cfg<double, 4, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<double, 4, 32, false>(A, L.ntiles, st);
+  } else if (A.Cp <= 2) {
+    rc = det ? launch_bwd_cfg<float, 2, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<float, 2, 32, false>(A, L.ntiles, st);
+  } else if (A.Cp <= 8) {
+    rc = det ? launch_bwd_cfg<float, 8, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<float, 8, 32, false>(A, L.ntiles, st);
+  } else if (A.Cp <= 16) {
+    rc = det ? launch_bwd_cfg<float, 16, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<float, 16, 32, false>(A, L.ntiles, st);
+  } else {
+    rc = det ? launch_bwd_cfg<float, 32, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<float, 32, 32, false>(A, L.ntiles, st);
+  }
+  if (rc != GSPARC_OK || !det) return rc;
+  RedArgs R;
+  R.pairs = A.pairs;
+  R.tile_start = A.tile_start;
+  R.wstop = A.wstop;
+  R.key = (const uint64_t*)(frame + L.off_key);
+  R.rect = (const int4*)(frame + L.off_rect);
+  R.dgc = A.dgc;
+  R.dgg = A.dgg;
+  R.gcoef = A.gcoef;
+  R.ggeo = A.ggeo;
+  R.n = L.n;
+  R.Cp = A.Cp;
+  R.nchunks = A.nchunks;
+  R.ntx = L.ntx;
+  R.nsub = A.nsub;
+  const unsigned blocks = (unsigned)((L.n + 7) / 8);
+  if (blocks == 0) return GSPARC_OK;
+  if (L.dtype == GSPARC_F64) k_bwd_reduce<double><<<blocks, 256, 0, st>>>(R);
+  else k_bwd_reduce<float><<<blocks, 256, 0, st>>>(R);
+  return check_launch("k_bwd_reduce");
 }
 
 }  // namespace gs

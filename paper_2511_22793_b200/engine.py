@@ -43,7 +43,7 @@ class Frame:
         L = _lib.CLayout()
         check(lib().gsparc_plan_frame(int(n), int(w), int(h), int(channels),
                                       int(pair_capacity), int(dtype_code_),
-                                      int(bool(with_backward)),
+                                      int(with_backward),
                                       ctypes.byref(L)))
         self.layout = L
         # zero-initialised once: coef rows of never-live Gaussians must be
@@ -53,7 +53,9 @@ class Frame:
         self.n, self.w, self.h = int(n), int(w), int(h)
         self.channels = int(channels)
         self.dtype_code = int(dtype_code_)
-        self.with_backward = bool(with_backward)
+        # 0: forward only, 1: backward (atomic accumulation), 2: backward
+        # with the deterministic fixed-order reduction buffers
+        self.with_backward = int(with_backward)
 
     @property
     def ptr(self):
@@ -183,6 +185,9 @@ class Renderer:
         positions|log_scales|rotations|raw_opacities|mlp_weights."""
         if not frame.with_backward:
             raise ValueError("frame was not planned with_backward")
+        if deterministic and frame.with_backward != 2:
+            raise ValueError("deterministic backward needs a frame planned "
+                             "with with_backward=2")
         n, P = cloud.n, cloud.P
         if grad is None:
             grad = torch.empty(n * (11 + P), dtype=_TORCH_DT[grad_dtype_code],

@@ -273,7 +273,8 @@ class Trainer:
         # size the pair buffer with one synchronous render
         self.tx.copy_(self.tx_all[:1].expand(self.Bl, 3))
         _, self.frame = self.R.forward(self.dev, pose, self.tx, self.w, self.h,
-                                       image=self.img, with_backward=True,
+                                       image=self.img,
+                                       with_backward=2 if cfg.deterministic else 1,
                                        lazy=False)
         self.graph = None
 
@@ -288,7 +289,7 @@ class Trainer:
         dimg, _ = self.loss.run(self.img, self.gt, self.sup,
                                 self.cfg.lambda_dssim)
         self.R.backward(self.dev, self.pose, self.tx, dimg, self.frame,
-                        grad=self.grad)
+                        grad=self.grad, deterministic=self.cfg.deterministic)
 
     def _update(self):
         _run_adam(self.dev, self.grad, self.state, self.cfg,

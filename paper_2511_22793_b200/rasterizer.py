@@ -198,9 +198,12 @@ def rasterize_forward(cloud, pose: ViewPose, tx, w, h, dtype=np.float32,
     dc = dtype_code(dtype)
     dev = _device_cloud(cloud, dc == _lib.F64)
     txs = _tx_tensor(tx)
+    # with_backward=2: the reference's backward is deterministic (bit-identical
+    # reruns, tests/test_acceptance.py:310-357), so the drop-in uses the
+    # fixed-order reduction
     img, frame = renderer().forward(dev, pose, txs, int(w), int(h),
                                     t_eps=t_eps, dtype_code_=dc,
-                                    with_backward=True, lazy=False)
+                                    with_backward=2, lazy=False)
     aux = RenderAux(frame, dev, pose, tx, dev.n, np.dtype(dtype).type,
                     t_eps, txs)
     return SpectrumImage(img[0]), aux
@@ -227,7 +230,8 @@ def rasterize_backward(dL_dimage, cloud, pose: ViewPose, tx,
                          .reshape(1, f.h, f.w, C), dtype=f.rdtype,
                          device="cuda")
     grad = renderer().backward(aux.cloud_dev, pose, aux.txs_dev, dL, f,
-                               grad_dtype_code=_lib.F64)
+                               grad_dtype_code=_lib.F64,
+                               deterministic=f.with_backward == 2)
     g = {k: v.cpu().numpy() for k, v in
          split_flat(grad, aux.cloud_dev.n, aux.cloud_dev.P).items()}
     return ParamGradients(**g)
@@ -246,7 +250,11 @@ def rasterize_forward_batch(cloud: DeviceCloud, pose: ViewPose, txs, w, h,
 
 
 def rasterize_backward_batch(dL, cloud: DeviceCloud, pose: ViewPose, txs,
-                             frame, grad=None):
-    """sum_b d<dL_b, img_b>/dparams into a flat f32 device buffer."""
+                             frame, grad=None, deterministic=None):
+    """sum_b d<dL_b, img_b>/dparams into a flat f32 device buffer.
+    deterministic (default: whether the frame was planned with
+    with_backward=2) selects the fixed-order reduction."""
+    if deterministic is None:
+        deterministic = frame.with_backward == 2
     return renderer().backward(cloud, pose, _tx_tensor(txs), dL, frame,
-                               grad=grad)
+                               grad=grad, deterministic=deterministic)

@@ -110,7 +110,27 @@ def fwd_case(name, cloud, tx, w, h, dtype=np.float32, t_eps=rasterizer.T_EPS,
     save(name, **out)
 
 
+def dup_case():
+    """Backward with a seam-duplicated Gaussian (rasterizer.py:139-141):
+    the reference accumulates per tile with g[rows] += ..., so only the
+    later copy's row survives (numpy last-write-wins).  Smallest seed whose
+    perturbed 64-Gaussian cloud has a duplicate at 180 x 45."""
+    tx = [0.3, 1.2, -0.8]
+    for seed in range(100, 400):
+        c = make_cloud(64, seed=seed)
+        _, aux = rasterize_forward(c, POSE, tx, 180, 45)
+        if any(len(set(r.tolist())) < len(r) for r in aux.tiles.values()):
+            print(f"bwd_dup: seed {seed}")
+            fwd_case("bwd_dup", c, tx, 180, 45, with_ref=False, dL_seed=23)
+            return
+    raise RuntimeError("no seam duplicate found")
+
+
 def main():
+    if sys.argv[1:] == ["--only", "bwd_dup"]:
+        dup_case()
+        return
+    dup_case()
     # --- known answers (tests/test_rasterizer.py:33-70)
     d = 2.0 * pixel_to_direction(18, 4, 36, 9)
     fwd_case("ka_single", single(d), [0.0, 0.0, 0.0], 36, 9)

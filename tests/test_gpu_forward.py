@@ -77,7 +77,7 @@ def assert_tiles_equal(aux, fx):
 
 
 GOLD = ["ka_single", "ka_two", "ka_clamp", "ka_near", "rand96_0", "rand96_1",
-        "rand96_2", "f64_noexit", "seam", "seam_dup", "bwd4", "bwd64",
+        "rand96_2", "f64_noexit", "seam", "seam_dup", "bwd4", "bwd64", "bwd_dup",
         "bench512"]
 
 

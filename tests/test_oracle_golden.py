@@ -9,7 +9,7 @@ from conftest import golden, golden_cloud, golden_dL
 
 FWD_CASES = ["ka_single", "ka_two", "ka_clamp", "ka_near", "rand96_0",
              "rand96_1", "rand96_2", "f64_noexit", "seam", "seam_dup",
-             "bwd4", "bwd64", "bench512"]
+             "bwd4", "bwd64", "bench512", "bwd_dup"]
 RX, W = np.zeros(3), np.eye(3)
 
 
@@ -60,7 +60,7 @@ def test_prepare_matches_reference(case):
 
 
 @pytest.mark.parametrize("case", ["rand96_0", "rand96_1", "rand96_2",
-                                  "bwd4", "bwd64", "bench512"])
+                                  "bwd4", "bwd64", "bench512", "bwd_dup"])
 def test_backward_matches_reference(case):
     fx = golden(case)
     cloud = golden_cloud(fx)
