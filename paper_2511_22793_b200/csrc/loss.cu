@@ -33,7 +33,8 @@ struct LossArgsT {
   double* H5;    // [5][NI][S][h][w]
   double* G3;    // [3][NI][S][h][w]
   double* A3;    // [3][NI][S][h][w]
-  double* sums;  // [NI][S+2]: ssim_c sums..., l1 sum, sq sum
+  double* sums;  // [NI * S][3] per-plane (ssim, l1, sq) sums
+  double* V3;    // [3][tot] per-pixel (ssim, l1, sq) terms
   double* stats; // [NI][4]
   int NI, S, C, h, w, sup;
   double lam;
@@ -114,26 +115,39 @@ __global__ void k_loss_v(LossArgsT<T> A) {
     l1_v = fabs(x - y);
     sq_v = (x - y) * (x - y);
   }
-  // per-(image, channel) sums: warp-reduce when the warp lies in one plane
-  const unsigned full = 0xffffffffu;
-  const int key = (e < tot) ? (b * A.S + s) : -1;
-  const int leader_key = __shfl_sync(full, key, 0);
-  const bool uniform = __all_sync(full, key == leader_key);
-  if (uniform) {
-    ssim_v = warp_sum(ssim_v);
-    l1_v = warp_sum(l1_v);
-    sq_v = warp_sum(sq_v);
-    if ((threadIdx.x & 31) == 0 && key >= 0) {
-      double* sm = A.sums + (int64_t)b * (A.S + 2);
-      atomicAdd(sm + s, ssim_v);
-      atomicAdd(sm + A.S, l1_v);
-      atomicAdd(sm + A.S + 1, sq_v);
-    }
-  } else if (key >= 0) {
-    double* sm = A.sums + (int64_t)b * (A.S + 2);
-    atomicAdd(sm + s, ssim_v);
-    atomicAdd(sm + A.S, l1_v);
-    atomicAdd(sm + A.S + 1, sq_v);
+  // per-pixel terms; summed per (image, channel) plane in a fixed order by
+  // k_loss_reduce (no float atomics: the reported losses are bit-stable)
+  if (e < tot) {
+    A.V3[e] = ssim_v;
+    A.V3[tot + e] = l1_v;
+    A.V3[2 * tot + e] = sq_v;
+  }
+}
+
+// one CTA per plane: strided per-thread sums, then a fixed shuffle tree
+template <typename T>
+__global__ void __launch_bounds__(256) k_loss_reduce(LossArgsT<T> A) {
+  __shared__ double s_part[8][3];
+  const int64_t plane = (int64_t)A.h * A.w, tot = (int64_t)A.NI * A.S * plane;
+  const int64_t p = blockIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < plane; i += blockDim.x) {
+    const int64_t e = p * plane + i;
+    v[0] += A.V3[e];
+    v[1] += A.V3[tot + e];
+    v[2] += A.V3[2 * tot + e];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) s_part[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w][threadIdx.x];
+    A.sums[p * 3 + threadIdx.x] = t;  // plane p = b * S + s
   }
 }
 
@@ -204,21 +218,25 @@ template <typename T>
 __global__ void k_loss_finalize(LossArgsT<T> A) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= A.NI) return;
-  const double* sm = A.sums + (int64_t)b * (A.S + 2);
+  const double* sm = A.sums + (int64_t)b * A.S * 3;
   const double n = (double)A.h * A.w;
-  double ss = 0.0;
-  for (int s = 0; s < A.S; ++s) ss += sm[s] / n;
+  double ss = 0.0, l1s = 0.0, sqs = 0.0;
+  for (int s = 0; s < A.S; ++s) {
+    ss += sm[3 * s] / n;
+    l1s += sm[3 * s + 1];
+    sqs += sm[3 * s + 2];
+  }
   ss /= A.S;
-  const double l1 = sm[A.S] / (n * A.S);
+  const double l1 = l1s / (n * A.S);
   A.stats[4 * b + 0] = (1.0 - A.lam) * l1 + A.lam * (1.0 - ss);
   A.stats[4 * b + 1] = l1;
   A.stats[4 * b + 2] = ss;
-  A.stats[4 * b + 3] = sm[A.S + 1] / (n * A.S);
+  A.stats[4 * b + 3] = sqs / (n * A.S);
 }
 
 int64_t loss_scratch_bytes(int NI, int h, int w, int C) {
   const int64_t tot = (int64_t)NI * C * h * w;  // upper bound: S <= C
-  return (int64_t)sizeof(double) * (11 * tot + (int64_t)NI * (C + 2)) + 256;
+  return (int64_t)sizeof(double) * (14 * tot + (int64_t)NI * C * 3) + 256;
 }
 
 template <typename T>
@@ -242,12 +260,12 @@ static int run_loss(const T* img, const T* gt, int NI, int h, int w, int C, int 
   A.H5 = base;
   A.G3 = A.H5 + 5 * tot;
   A.A3 = A.G3 + 3 * tot;
-  A.sums = A.A3 + 3 * tot;
-  if (cudaMemsetAsync(A.sums, 0, sizeof(double) * NI * (A.S + 2), st) != cudaSuccess)
-    return check_launch("loss memset");
+  A.V3 = A.A3 + 3 * tot;
+  A.sums = A.V3 + 3 * tot;
   const unsigned blocks = (unsigned)((tot + 255) / 256);
   k_loss_h<T><<<blocks, 256, 0, st>>>(A);
   k_loss_v<T><<<blocks, 256, 0, st>>>(A);
+  k_loss_reduce<T><<<(unsigned)(NI * A.S), 256, 0, st>>>(A);
   k_loss_adj_v<T><<<blocks, 256, 0, st>>>(A);
   k_loss_adj_h<T><<<blocks, 256, 0, st>>>(A);
   k_loss_finalize<T><<<(NI + 127) / 128, 128, 0, st>>>(A);

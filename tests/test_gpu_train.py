@@ -157,3 +157,35 @@ def test_trainer_graph_replay_equals_eager(OPT):
         x = getattr(a.dev, k).double().cpu().numpy()
         y = getattr(b.dev, k).double().cpu().numpy()
         assert np.abs(x - y).max() <= 1e-5 * max(1.0, np.abs(x).max())
+
+
+def test_deterministic_training_is_bit_identical(OPT):
+    """The reference's determinism contract (tests/test_acceptance.py:310-357:
+    identical runs give bit-identical checkpoints and metrics): with
+    TrainConfig(deterministic=True) the backward uses the fixed-order
+    reduction and the loss statistics a fixed-order sum, so two runs (one
+    eager, one CUDA-graph replay) agree bit for bit in every parameter and
+    every reported loss."""
+    import torch
+    from paper_2511_22793_b200 import GaussianCloud, ViewPose
+    w, h, B = 90, 30, 4
+    oc = O.round_f32(O.perturbed_scene(400, seed=12))
+    txs = O.sample_tx(13, 16)
+    gts = np.random.default_rng(4).random((16, h, w, 1)) * 0.3
+    cfg = OPT.TrainConfig(width=w, height=h, batch_tx=B, deterministic=True)
+    mk = lambda: GaussianCloud(*(getattr(oc, k).copy() for k in O.GROUPS))
+    runs = []
+    for graph in (False, True):
+        tr = OPT.Trainer(mk(), ViewPose(np.zeros(3)), cfg, txs, gts)
+        if graph:
+            tr.capture()
+        losses = [tr.step(bt).cpu().numpy().copy()
+                  for bt in ([0, 1, 2, 3], [4, 5, 6, 7], [3, 9, 12, 15])]
+        torch.cuda.synchronize()
+        assert tr.check()
+        runs.append((losses, {k: getattr(tr.dev, k).cpu().numpy().copy()
+                              for k in O.GROUPS}))
+    for la, lb in zip(runs[0][0], runs[1][0]):
+        assert np.array_equal(la, lb)
+    for k in O.GROUPS:
+        assert np.array_equal(runs[0][1][k], runs[1][1][k]), k
