@@ -293,27 +293,42 @@ def run_ours(args):
     renders = world * args.steps * B
     value = renders / (total_ms / 1e3)
 
-    # ---- end-to-end through the public API (host TX in, host image out)
-    pin_tx = torch.empty((B, 3), dtype=torch.float64).pin_memory()
-    pin_img = torch.empty((B, h, w, C), dtype=torch.float32).pin_memory()
+    # ---- end-to-end through the public API (host TX in, host image out).
+    # Renders run on the compute stream, each image's D2H on a copy stream
+    # (double-buffered device images), so the copy of render i overlaps
+    # render i+1 -- what a serving loop would do.  Every render's TX is
+    # copied in from pinned memory and every image lands in pinned memory
+    # inside the timed region.
+    pin_tx = [torch.empty((B, 3), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pin_img = [torch.empty((B, h, w, C), dtype=torch.float32).pin_memory() for _ in range(2)]
+    dev_img = [img, torch.empty_like(img)]
+    copy_stream = torch.cuda.Stream()
+    rendered = [torch.cuda.Event() for _ in range(2)]
+    copied = [torch.cuda.Event() for _ in range(2)]
     e2e_steps = min(args.steps, 100)
+
+    def e2e_run(n):
+        for i in range(n):
+            k = i & 1
+            t = i % total_steps
+            pin_tx[k].copy_(torch.as_tensor(txs_np[t * B:(t + 1) * B]))
+            stream.wait_event(copied[k])          # image buffer k is free again
+            tx_dev = pin_tx[k].to("cuda", non_blocking=True)
+            out, _ = rasterize_forward_batch(dc, pose, tx_dev, w, h, lazy=lazy,
+                                             frame=frame, image=dev_img[k])
+            rendered[k].record(stream)
+            copy_stream.wait_event(rendered[k])
+            with torch.cuda.stream(copy_stream):
+                pin_img[k].copy_(out, non_blocking=True)
+                copied[k].record(copy_stream)
+
+    e2e_run(4)
+    torch.cuda.synchronize()
     e_s = torch.cuda.Event(enable_timing=True)
     e_e = torch.cuda.Event(enable_timing=True)
-    for i in range(3):
-        k = i % total_steps
-        pin_tx.copy_(torch.as_tensor(txs_np[k * B:(k + 1) * B]))
-        out, _ = rasterize_forward_batch(dc, pose, pin_tx, w, h, lazy=lazy,
-                                         frame=frame, image=img)
-        pin_img.copy_(out, non_blocking=True)
-    torch.cuda.synchronize()
     e_s.record(stream)
-    for i in range(e2e_steps):
-        pin_tx.copy_(torch.as_tensor(txs_np[(i % total_steps) * B:
-                                            (i % total_steps + 1) * B]))
-        tx_dev = pin_tx.to("cuda", non_blocking=True)
-        out, _ = rasterize_forward_batch(dc, pose, tx_dev, w, h, lazy=lazy,
-                                         frame=frame, image=img)
-        pin_img.copy_(out, non_blocking=True)
+    e2e_run(e2e_steps)
+    stream.wait_stream(copy_stream)
     e_e.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e_s.elapsed_time(e_e) / e2e_steps
@@ -350,8 +365,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": 24 * B,
                     "d2h_bytes_per_step": img_bytes,
                     "ms_per_step": e2e_ms,
-                    "path": "rasterize_forward_batch(host TX) + D2H of the "
-                            "image into pinned memory"},
+                    "path": "rasterize_forward_batch(pinned host TX -> device) "
+                            "+ D2H of every image into pinned memory on a copy "
+                            "stream overlapping the next render"},
             "gpu_launches": int(args.steps * kernels_per_step(lazy)),
             "roofline": roof,
             "pipeline_hbm": {"algorithmic_bytes": bytes_fwd,
