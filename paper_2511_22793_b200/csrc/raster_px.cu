@@ -407,10 +407,10 @@ struct PxbCfg {
   static constexpr uint32_t D_COLS = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : 256;
   static constexpr uint32_t A_COL0 = D_COLS;
   static constexpr uint32_t TMEM_COLS = D_COLS + 128 <= 256 ? 256 : 512;
-  static constexpr int THREADS = 288;                  // 8 weight warps + MMA warp
+  static constexpr int THREADS = 256;                  // 2 groups x 4 weight warps
   static constexpr int MIN_CTAS = TMEM_COLS == 256 ? 2 : 1;
-  // two CTAs of 9 warps must fit the 64K-register file (ncu: 112 leaves one)
-  static constexpr int MAXREG = MIN_CTAS == 2 ? 96 : 224;
+  // 16K registers per SM sub-partition: 2 CTAs x 8 warps = 4 warps each
+  static constexpr int MAXREG = MIN_CTAS == 2 ? 128 : 224;
   static constexpr int PPR = NA * 8;                   // 16 B pieces per coef row
   static constexpr int NPF = (PX_K * PPR + 127) / 128; // pieces per group thread
 };
@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   __shared__ __align__(16) float4 s_rec[8][2 * PX_K];  // per weight warp
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_done;
   __shared__ uint32_t s_tmem;
+  __shared__ int s_next;  // next chunk whose MMAs may be issued (order token)
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const long long t_start = clock64();
@@ -460,9 +461,10 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       mbar_init(&s_empty[k], 1);
     }
     mbar_init(&s_done, 1);
+    s_next = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem)),
                  "r"(CF::TMEM_COLS));
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
 
   if (warp < 8) {
     // ---------------- weight groups: group gq takes chunks c = gq (mod 2)
@@ -488,6 +491,10 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     const uint32_t a_lo = a_hi + 32;
     unsigned char* bhi = sB + gq * CF::STAGE;
     unsigned char* blo = bhi + CF::PLANE;
+    // instruction descriptor: D f32, A/B tf32, A K-major, B MN-major,
+    // N = NP, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
+                           ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const bool vec = (A.Cp & 3) == 0;
     const int ncol = (int)min((int64_t)NP, A.Cp - col0);   // channels of this CTA
     const int ppr = (ncol + 3) >> 2;                        // pieces with channels
@@ -510,8 +517,23 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       float T = nT;
       const uint32_t used = nused;
       __syncwarp();  // previous chunk's readers are done with rs
-      rs[2 * lane] = n0;
-      rs[2 * lane + 1] = n1;
+      // compact the chunk's used entries (pass-A mask: at least one pixel of
+      // the CTA includes them) to the front, in list order.  Skipping an
+      // unused entry is exact: every pixel that is still live sees alpha = 0
+      // there.  The K order of the MMA is free as long as A columns and B
+      // rows agree, so column j is the j-th used entry; the rest are zero.
+      const int nu = __popc(used);
+      {
+        if (lane >= nu) {  // padding slots: zero opacity, alpha = 0
+          rs[2 * lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+          rs[2 * lane + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+        }
+        if ((used >> lane) & 1u) {  // used entries, in list order
+          const int slot = __popc(used & ((1u << lane) - 1u));
+          rs[2 * slot] = n0;
+          rs[2 * slot + 1] = n1;
+        }
+      }
       prefetch(c + 2);
       __syncwarp();
       // coef rows of the used entries, issued now and consumed after the
@@ -523,7 +545,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         const int p = gt + 128 * u;
         const int e = p / CF::PPR, jj = p - e * CF::PPR;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < PX_K && jj < ppr && ((used >> e) & 1u)) {
+        if (e < nu && jj < ppr) {
           const int idx = __float_as_int(rs[2 * e + 1].w);
           if (idx >= 0) {
             const float* row = A.coef + (int64_t)idx * A.Cp + col0 + 4 * jj;
@@ -542,17 +564,20 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       }
       const long long t0 = clock64();
       float wv[PX_K];
+#pragma unroll
+      for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
       if (__any_sync(0xffffffffu, T >= teps)) {
 #pragma unroll
-        for (int e = 0; e < PX_K; ++e) {
-          const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
-          const bool act = T >= teps && a > 0.f;
-          wv[e] = act ? T * a : 0.f;
-          T = act ? T * (1.f - a) : T;
-        }
-      } else {
+        for (int e0 = 0; e0 < PX_K; e0 += 8) {
+          if (e0 >= nu) break;  // uniform: groups of 8 keep the ILP
 #pragma unroll
-        for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
+          for (int e = e0; e < e0 + 8; ++e) {
+            const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
+            const bool act = T >= teps && a > 0.f;
+            wv[e] = act ? T * a : 0.f;
+            T = act ? T * (1.f - a) : T;
+          }
+        }
       }
       const long long t1 = clock64();
       if (k >= 1) mbar_wait_sleep(&s_empty[gq], (k - 1) & 1);
@@ -577,7 +602,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       for (int u = 0; u < CF::NPF; ++u) {
         const int p = gt + 128 * u;
         const int e = p / CF::PPR, jj = p - e * CF::PPR;
-        if (e < PX_K && jj < ppr && ((used >> e) & 1u)) {
+        if (e < nu && jj < ppr) {
           const float4 x = cv[u];
           float4 h;
           h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -594,44 +619,45 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_full[gq]);
+      if (q == 0 && lane == 0) {
+        // this group's leader issues the chunk's MMAs once all 4 warps have
+        // staged it, in chunk order (token), so the accumulation order --
+        // and the image -- is the same on every run
+        mbar_wait(&s_full[gq], k & 1);
+        while (*(volatile int*)&s_next != c) {
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ma_hi = tmem + CF::A_COL0 + 64 * gq, ma_lo = ma_hi + 32;
+        const uint32_t mb_hi = smem_u32(bhi), mb_lo = mb_hi + CF::PLANE;
+#pragma unroll
+        for (int ks = 0; ks < PX_K / 8; ++ks) {
+          const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
+          const uint32_t ko = ks * CF::NA * 1024;  // 8 entries = 2 atom rows of K
+          mma_tf32_ts(tmem, ma_hi + 8 * ks, umma_desc_mn_b32(mb_hi + ko, CF::NA * 512), idesc,
+                      acc0);
+          mma_tf32_ts(tmem, ma_hi + 8 * ks, umma_desc_mn_b32(mb_lo + ko, CF::NA * 512), idesc,
+                      1u);
+          mma_tf32_ts(tmem, ma_lo + 8 * ks, umma_desc_mn_b32(mb_hi + ko, CF::NA * 512), idesc,
+                      1u);
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&s_empty[gq]))
+            : "memory");
+        if (c == nch - 1)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  smem_u32(&s_done))
+              : "memory");
+        __threadfence_block();
+        *(volatile int*)&s_next = c + 1;
+      }
+      __syncwarp();
     }
     if (A.dbg && lane == 0 && q == 0) {
       A.dbg[blockIdx.x * 16 + 6 + gq] = tw;
       A.dbg[blockIdx.x * 16 + 8 + gq] = tc;
     }
-  } else if (lane == 0) {
-    // ---------------- MMA issuer (warp 8)
-    // instruction descriptor: D f32, A/B tf32, A K-major, B MN-major,
-    // N = NP, M = 128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
-                           ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    long long twa = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int s = c & 1;
-      const long long t0 = clock64();
-      mbar_wait(&s_full[s], (c >> 1) & 1);
-      twa += clock64() - t0;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_hi = tmem + CF::A_COL0 + 64 * s, a_lo = a_hi + 32;
-      const uint32_t b_hi = smem_u32(sB + s * CF::STAGE), b_lo = b_hi + CF::PLANE;
-#pragma unroll
-      for (int ks = 0; ks < PX_K / 8; ++ks) {
-        const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
-        const uint32_t ko = ks * CF::NA * 1024;  // 8 entries = 2 atom rows of K
-        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_mn_b32(b_hi + ko, CF::NA * 512), idesc, acc0);
-        mma_tf32_ts(tmem, a_hi + 8 * ks, umma_desc_mn_b32(b_lo + ko, CF::NA * 512), idesc, 1u);
-        mma_tf32_ts(tmem, a_lo + 8 * ks, umma_desc_mn_b32(b_hi + ko, CF::NA * 512), idesc, 1u);
-      }
-      asm volatile(
-          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              smem_u32(&s_empty[s]))
-          : "memory");
-    }
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&s_done))
-        : "memory");
-    if (A.dbg) A.dbg[blockIdx.x * 16 + 0] = twa;
   }
 
   // ---------------- epilogue: warps 0..3 own TMEM lanes 32q.. (= pixels)
@@ -643,6 +669,8 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       mbar_wait_sleep(&s_done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    const long long te0 = clock64();
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = te0 - t_start;
     const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < NP; c0 += 8) {
@@ -682,7 +710,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(CF::TMEM_COLS));
   }

@@ -20,7 +20,7 @@ host = (ctypes.c_longlong * (n * 16))()
 assert L.gsparc_debug_copy(host, ctypes.c_int64(n * 16)) == 0
 d = np.ctypeslib.as_array(host).reshape(n, 16)
 names = ["mma_wait", "", "", "", "", "", "w0_waitE", "w1_waitE", "w0_comp", "w1_comp",
-         "total", "nch"]
+         "total", "nch", "", "t_prologue_end", "t_epilogue_start"]
 order = np.argsort(-d[:, 10])
 print("avg:", {k: int(d[:, i].mean()) for i, k in enumerate(names)})
 for r in order[:6]:
