@@ -295,6 +295,9 @@ constexpr int RS_T = 1024;
 constexpr int RS_W = RS_T / 32;
 constexpr int RS_E = 8;
 constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
+constexpr int BK_BITS = 12;          // bucket pass: top 12 bits of the key
+constexpr int BK_N = 1 << BK_BITS;
+constexpr int BK_BIG = 64;           // larger buckets -> LSD radix fallback
 
 __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n,
                                       uint32_t cmin, int shift, int npass) {
@@ -418,10 +421,89 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* 
     __syncthreads();
     const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
     const int bits = span ? 32 - __clz(span) : 0;
-    const int shift = bits > 24 ? bits - 24 : 0;
-    const int npass = (bits - shift + 7) / 8;  // 0..3
-    uint64_t* r = block_radix_sort(a, b, cnt, n, cmin, shift, npass);
-    fix_coarse_ties(r, n, key, cmin, shift);
+    // one bucket pass on the top 12 bits of the tile-relative coarse key
+    // (shared-memory atomics; order inside a bucket is fixed next), then
+    // every bucket is insertion-sorted by (coarse32, index) and runs tying
+    // on coarse32 are put in exact (f64 key, index) order
+    const int bshift = bits > BK_BITS ? bits - BK_BITS : 0;
+    int* bcnt = cnt;              // [BK_N]
+    int* bcur = cnt + BK_N;       // [BK_N]
+    __shared__ int s_bmax;
+    if (threadIdx.x == 0) s_bmax = 0;
+    for (int t = threadIdx.x; t < BK_N; t += blockDim.x) bcnt[t] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const int bk = (int)(((uint32_t)(a[j] >> 32) - cmin) >> bshift);
+      const int c = atomicAdd(bcnt + bk, 1);
+      if (c == BK_BIG) atomicMax(&s_bmax, c);
+    }
+    __syncthreads();
+    uint64_t* r;
+    if (s_bmax < BK_BIG) {
+      // exclusive scan of the bucket counts (BK_N / blockDim per thread)
+      constexpr int PER = BK_N / RS_T;
+      int loc[PER];
+      int sum = 0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        loc[k] = sum;
+        sum += bcnt[threadIdx.x * PER + k];
+      }
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      __shared__ int s_wsum[RS_W];
+      if (lane == 31) s_wsum[wid] = inc;
+      __syncthreads();
+      if (wid == 0) {
+        int x = s_wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += u;
+        }
+        s_wsum[lane] = x;
+      }
+      __syncthreads();
+      const int base0 = inc - sum + (wid > 0 ? s_wsum[wid - 1] : 0);
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int st0 = base0 + loc[k];
+        bcur[threadIdx.x * PER + k] = st0;
+        bcnt[threadIdx.x * PER + k] = st0;  // bucket start
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const uint64_t v = a[j];
+        const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
+        b[atomicAdd(bcur + bk, 1)] = v;
+      }
+      __syncthreads();
+      for (int bk = threadIdx.x; bk < BK_N; bk += blockDim.x) {
+        const int lo = bcnt[bk], hi = bcur[bk];
+        for (int p = lo + 1; p < hi; ++p) {  // insertion sort, buckets are small
+          const uint64_t v = b[p];
+          int q = p - 1;
+          while (q >= lo && b[q] > v) {
+            b[q + 1] = b[q];
+            --q;
+          }
+          b[q + 1] = v;
+        }
+      }
+      __syncthreads();
+      r = b;
+      fix_coarse_ties(r, n, key);
+    } else {  // a heavily populated bucket: stable LSD radix passes
+      const int shift = bits > 24 ? bits - 24 : 0;
+      const int npass = (bits - shift + 7) / 8;  // 0..3
+      r = block_radix_sort(a, b, cnt, n, cmin, shift, npass);
+      fix_coarse_ties(r, n, key, cmin, shift);
+    }
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = r[j];
   } else if (n > RS_CAP) {

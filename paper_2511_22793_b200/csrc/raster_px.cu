@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   __shared__ int s_ndone, s_nch, s_stop[4];
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const long long t_startA = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CtaGeom g = cta_geom(A, blockIdx.x);
   const int start = A.tile_start[g.tile];
@@ -169,9 +170,12 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     // ---------------- producer: scan, cull, compact into the ring
     const unsigned lt = (1u << lane) - 1u;
     int c = 0, fill = 0, acquired = 0;
+    long long tpe = 0;
     auto acquire = [&](int k) {
       if (k > acquired) {
+        const long long t0 = clock64();
         if (k >= PX_RING) mbar_wait(&s_empty[k % PX_RING], ((k / PX_RING) - 1) & 1);
+        tpe += clock64() - t0;
         acquired = k;
       }
     };
@@ -266,6 +270,11 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     }
     acquire(c);
     publish(c, -1);  // end of list
+    if (A.dbg && lane == 0) {
+      A.dbg[blockIdx.x * 16 + 0] = tpe;
+      A.dbg[blockIdx.x * 16 + 1] = clock64() - t_startA;
+      A.dbg[blockIdx.x * 16 + 2] = c;
+    }
   } else {
     // ---------------- consumers: one pixel per lane
     const int px = g.x0 + (lane & 15), py = g.y0 + 2 * warp + (lane >> 4);
@@ -279,11 +288,15 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     for (int ch = 0; ch < SCW; ++ch) acc[ch] = 0.f;
     bool wdone = !__any_sync(0xffffffffu, T >= teps);
     if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
+    long long twf = 0, tcc = 0;
     for (int c = 0;; ++c) {
       const int s = c % PX_RING;
+      const long long tf0 = clock64();
       mbar_wait(&s_full[s], (c / PX_RING) & 1);
+      twf += clock64() - tf0;
       const int n = *(volatile int*)&s_hdr[s];
       if (n < 0) break;
+      const long long tc0 = clock64();
       A.ch_T[(slot0 + c) * 128 + warp * 32 + lane] = T;  // checkpoint for pass B
       if (!wdone) {
         unsigned actm = 0;
@@ -317,8 +330,13 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         wdone = !__any_sync(0xffffffffu, T >= teps);
         if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
       }
+      tcc += clock64() - tc0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[s]);
+    }
+    if (A.dbg && lane == 0) {
+      A.dbg[blockIdx.x * 16 + 3 + warp] = twf;
+      A.dbg[blockIdx.x * 16 + 7 + warp] = tcc;
     }
     if (inside) {
       const int q = py * A.w + px;
@@ -341,6 +359,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   }
   __syncthreads();
   if (threadIdx.x == 0) A.ch_n[blockIdx.x] = s_nch;
+  if (A.dbg && threadIdx.x == 0) {
+    A.dbg[blockIdx.x * 16 + 11] = clock64() - t_startA;
+    A.dbg[blockIdx.x * 16 + 12] = s_nch;
+  }
   // live list (for the lazy MLP): entries of this CTA's chunks with an
   // included contribution; the first CTA to flag a Gaussian appends it.
   // Done once per CTA, off the per-chunk critical path.
@@ -737,6 +759,7 @@ static void launch_pxb(const PxArgs& A, int chunks_y, cudaStream_t st) {
     attr = true;
   }
   PxArgs B = A;
+  B.dbg = nullptr;
   static long long* dbg = nullptr;
   if (getenv("GSPARC_PXB_DBG")) {  // experiments only
     if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * 4096);
@@ -788,6 +811,13 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                      int pass, void* img, cudaStream_t st) {
   PxArgs A = make_px_args(L, frame, n_tx, C, t_eps, img);
   const int64_t Cp = A.Cp;
+  if (pass != 2 && getenv("GSPARC_PXA_DBG")) {  // experiments only: pass-A timing
+    static long long* dbga = nullptr;
+    if (!dbga) cudaMalloc(&dbga, sizeof(long long) * 16 * 4096);
+    cudaMemsetAsync(dbga, 0, sizeof(long long) * 16 * 4096, st);
+    A.dbg = dbga;
+    gsparc_dbg_ptr = dbga;
+  }
   if (pass != 2) {
     if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
       return check_launch("raster live memset");
