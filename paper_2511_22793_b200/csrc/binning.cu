@@ -295,7 +295,7 @@ constexpr int RS_T = 1024;
 constexpr int RS_W = RS_T / 32;
 constexpr int RS_E = 8;
 constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
-constexpr int BK_BITS = 12;          // bucket pass: top 12 bits of the key
+constexpr int BK_BITS = 13;          // bucket pass: top 13 bits of the key
 constexpr int BK_N = 1 << BK_BITS;
 constexpr int BK_BIG = 64;           // larger buckets -> LSD radix fallback
 
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* 
     __syncthreads();
     const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
     const int bits = span ? 32 - __clz(span) : 0;
-    // one bucket pass on the top 12 bits of the tile-relative coarse key
+    // one bucket pass on the top 13 bits of the tile-relative coarse key
     // (shared-memory atomics; order inside a bucket is fixed next), then
     // every bucket is insertion-sorted by (coarse32, index) and runs tying
     // on coarse32 are put in exact (f64 key, index) order
@@ -543,7 +543,8 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   size_t smem = sizeof(int) * (3 * (size_t)L.ntiles + 1 + 40);
   k_bin<<<blocks, 256, smem, st>>>(A);
   GS_TRY(check_launch("k_bin"));
-  const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * (RS_W * 256 + 512);
+  const size_t smem_sort =
+      2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * (size_t)max(RS_W * 256 + 512, 2 * BK_N);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
