@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GSPARC_ABI_VERSION 2
+#define GSPARC_ABI_VERSION 3
 
 enum {
   GSPARC_OK = 0,
@@ -104,8 +104,8 @@ typedef struct gsparc_frame_layout {
   int64_t off_rec64;      /* f64  [n,8] raster record (dtype f64 only)  */
   int64_t off_rect;       /* i32  [n,4] tile rectangle + pair count     */
   int64_t off_counters;   /* i32  [16]                                  */
-  int64_t off_tile_count; /* i32  [ntiles]                              */
-  int64_t off_tile_cursor;/* i32  [ntiles]                              */
+  int64_t off_tile_count; /* i32  [ntiles] pairs per tile               */
+  int64_t off_tile_cursor;/* i32  [ntiles] staged segments per tile     */
   int64_t off_tile_start; /* i32  [ntiles+1]                            */
   int64_t off_tile_stop;  /* i32  [ntiles*4] list prefix visited per sub-tile */
   int64_t off_pairs;      /* u64  [pair_capacity] per-tile sorted lists */
@@ -137,6 +137,12 @@ typedef struct gsparc_frame_layout {
                              (with_backward == 2: deterministic backward) */
   int64_t off_det_ggeo;   /* dtype [pair_capacity,4,max(1,ceil(ch/4)),6]
                              geometric partials (with_backward == 2)      */
+  int64_t off_stage;      /* u64  [pair_capacity] unsorted pairs staged
+                             by gsparc_prepare, one contiguous segment per
+                             (preprocess CTA, tile)                       */
+  int64_t off_seg;        /* i32  [ntiles,seg_stride,2] staged segments
+                             {stage offset, length} per tile              */
+  int64_t seg_stride;     /* segment slots per tile (preprocess CTAs)     */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);
@@ -153,8 +159,10 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height,
 int gsparc_prepare(const gsparc_cloud* cloud, const gsparc_view* view,
                    void* frame, const gsparc_frame_layout* L, void* stream);
 
-/* K3: bin into 16x16 tiles (incl. the azimuth-seam duplicate) and sort
- * every tile list by (radial depth, source index), bit-exact. */
+/* K3: sort every tile list by (radial depth, source index), bit-exact.
+ * gsparc_prepare has already binned the kept Gaussians into 16x16 tiles
+ * (incl. the azimuth-seam duplicate) as staged segments; this gathers each
+ * tile's segments, sorts them and writes pairs/tile_start. */
 int gsparc_bin_tiles(void* frame, const gsparc_frame_layout* L, void* stream);
 
 /* K1: coef[i, b*C + c] = MLP_i(tx_b, theta_i, phi_i)[c] / max(|mu_i-tx_b|, .05)

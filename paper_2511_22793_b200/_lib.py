@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsparc_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
 F32, F64 = 0, 1
@@ -51,7 +51,8 @@ class CLayout(ctypes.Structure):
                                       "dtype", "with_backward", "reserved")] +
                 [("off_" + k, c_i64) for k in _LAYOUT_OFFSETS] +
                 [("ch_slots", c_i64), ("off_ch_used", c_i64),
-                 ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64)])
+                 ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64),
+                 ("off_stage", c_i64), ("off_seg", c_i64), ("seg_stride", c_i64)])
 
 
 class CAdamConfig(ctypes.Structure):

@@ -1,137 +1,36 @@
-// K3: tile binning and per-tile depth sort.  Replaces the np.lexsort depth
-// order (rasterizer.py:82-87) and rasterizer._tile_lists
+// K3: per-tile depth sort.  Replaces the np.lexsort depth order
+// (rasterizer.py:82-87) restricted to each of rasterizer._tile_lists
 // (rasterizer.py:115-145).
 //
-// This is an MSD radix sort on the composite key (tile, depth, index):
-//   digit 1 (tile) -- counting sort: per-tile counts come from K2, an
-//     exclusive scan gives the tile ranges, every Gaussian is scattered into
-//     the buckets of the tiles its footprint covers (the azimuth-seam
-//     duplicate included: a tile covered by both column segments gets two
-//     entries, rasterizer.py:139-141);
-//   digits 2.. (depth, index) -- every bucket is sorted in shared memory by
-//     the packed key (coarse_depth32 << 32 | index).  coarse_depth32 is the
-//     monotone truncation (bits(depth) - bits(0.05)) >> 24; runs that tie on
-//     it are re-ordered by the full f64 bit pattern, so the final order is
-//     exactly np.lexsort((idx, depth)) restricted to the tile.
+// This is the second half of an MSD radix sort on the composite key
+// (tile, depth, index):
+//   digit 1 (tile) -- counting sort, done by K2 (preprocess.cu): every
+//     preprocess CTA stages its pairs as one contiguous segment per touched
+//     tile (the azimuth-seam duplicate included: a tile covered by both
+//     column segments gets two entries, rasterizer.py:139-141);
+//   digits 2.. (depth, index) -- one CTA per tile gathers the tile's
+//     segments into shared memory and sorts them by the packed key
+//     (coarse_depth32 << 32 | index).  coarse_depth32 is the monotone
+//     truncation (bits(depth) - bits(0.05)) >> 24; runs that tie on it are
+//     re-ordered by the full f64 bit pattern, so the final order is exactly
+//     np.lexsort((idx, depth)) restricted to the tile.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace gs {
 
-struct BinArgs {
-  const uint64_t* key;
-  const int4* rect;
-  const int* tile_count;
-  int* tile_cursor;
-  int* tile_start;
-  int* counters;
+struct SortArgs {
   uint64_t* pairs;
-  int64_t capacity;
-  int64_t n;
-  int ntx, ntiles;
+  int* tile_start;
+  const uint64_t* key;
+  int* counters;
+  const int* tile_count;
+  const int* tile_cursor;
+  const int2* seg;
+  const uint64_t* stage;
+  int64_t seg_stride;
+  int ntiles;
 };
-
-__device__ __forceinline__ uint32_t coarse_key(uint64_t k) {
-  return (uint32_t)((k - DEPTH_KEY_BASE) >> COARSE_SHIFT);
-}
-
-// Block-wide exclusive scan of `in[0..n)` into `out[0..n]` (out[n] = total),
-// any n, blockDim multiple of 32.  Uses `tmp` of blockDim/32+1 ints.
-__device__ void block_exclusive_scan(const int* in, int* out, int n, int* tmp) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (n + nt - 1) / nt;
-  const int beg = min(n, tid * per), end = min(n, beg + per);
-  int local = 0;
-  for (int k = beg; k < end; ++k) local += in[k];
-  // inclusive warp scan of `local`
-  int lane = tid & 31, warp = tid >> 5;
-  int v = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += u;
-  }
-  if (lane == 31) tmp[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    int nw = nt >> 5;
-    int w = lane < nw ? tmp[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += u;
-    }
-    if (lane < nw) tmp[lane] = w;  // inclusive warp totals
-  }
-  __syncthreads();
-  int run = v - local + (warp > 0 ? tmp[warp - 1] : 0);
-  for (int k = beg; k < end; ++k) {
-    out[k] = run;
-    run += in[k];
-  }
-  if (tid == nt - 1) out[n] = run;
-  __syncthreads();
-}
-
-__device__ __forceinline__ void unpack_rect(int4 r, int& y0, int& y1, int& a0, int& a1, int& b0,
-                                            int& b1) {
-  y0 = r.x & 0xffff;
-  y1 = r.x >> 16;
-  a0 = r.y & 0xffff;
-  a1 = r.y >> 16;
-  b0 = r.z & 0xffff;
-  b1 = r.z >> 16;
-}
-
-__global__ void __launch_bounds__(256) k_bin(BinArgs A) {
-  extern __shared__ int sm[];
-  const int T = A.ntiles;
-  int* s_start = sm;             // T+1
-  int* s_cnt = s_start + T + 1;  // T
-  int* s_base = s_cnt + T;       // T
-  int* s_tmp = s_base + T;       // 33
-  block_exclusive_scan(A.tile_count, s_start, T, s_tmp);
-  const int total = s_start[T];
-  if (blockIdx.x == 0) {
-    for (int t = threadIdx.x; t <= T; t += blockDim.x) A.tile_start[t] = s_start[t];
-    if (threadIdx.x == 0 && total > A.capacity) A.counters[GSPARC_CNT_OVERFLOW] = 1;
-  }
-  if (total > A.capacity) return;  // host reports the overflow
-  for (int t = threadIdx.x; t < T; t += blockDim.x) s_cnt[t] = 0;
-  __syncthreads();
-
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t k = (i < A.n) ? A.key[i] : ~0ULL;
-  const bool kept = k != ~0ULL;
-  int y0 = 0, y1 = -1, a0 = 0, a1 = -1, b0 = 0, b1 = -1;
-  if (kept) {
-    unpack_rect(A.rect[i], y0, y1, a0, a1, b0, b1);
-    for (int ty = y0; ty <= y1; ++ty) {
-      for (int tx = a0; tx <= a1; ++tx) atomicAdd(s_cnt + ty * A.ntx + tx, 1);
-      for (int tx = b0; tx <= b1; ++tx) atomicAdd(s_cnt + ty * A.ntx + tx, 1);
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    int c = s_cnt[t];
-    s_base[t] = c ? s_start[t] + atomicAdd(A.tile_cursor + t, c) : 0;
-    s_cnt[t] = 0;
-  }
-  __syncthreads();
-  if (kept) {
-    const uint64_t packed = ((uint64_t)coarse_key(k) << 32) | (uint32_t)i;
-    for (int ty = y0; ty <= y1; ++ty) {
-      for (int tx = a0; tx <= a1; ++tx) {
-        int t = ty * A.ntx + tx;
-        A.pairs[s_base[t] + atomicAdd(s_cnt + t, 1)] = packed;
-      }
-      for (int tx = b0; tx <= b1; ++tx) {
-        int t = ty * A.ntx + tx;
-        A.pairs[s_base[t] + atomicAdd(s_cnt + t, 1)] = packed;
-      }
-    }
-  }
-}
 
 // Ascending-only bitonic network on n elements (virtual +inf padding up to
 // the next power of two never moves, so no padding is stored).
@@ -382,35 +281,60 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
   return src;  // buffer holding the result
 }
 
-// Sort each tile's bucket by (coarse depth, index), fix coarse ties by the
-// full f64 key, then stage the f32 raster record of every entry in list
-// order (pair_rec) so the raster streams records instead of gathering them.
-__global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* tile_start,
-                                                    const uint64_t* key, int* counters,
-                                                    const float4* rec32, float4* pair_rec,
-                                                    int /*unused*/) {
+// Gather each tile's staged segments, sort them by (coarse depth, index),
+// fix coarse ties by the full f64 key and write the tile's list.
+__global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
-  if (counters[GSPARC_CNT_OVERFLOW]) return;
+  __shared__ int s_start[2];
+  __shared__ int s_pos;
+  __shared__ uint32_t s_mm[2];
   const int t = blockIdx.x;
-  const int s = tile_start[t], n = tile_start[t + 1] - s;
-  uint64_t* g = pairs + s;
-  if (n > 1 && n <= RS_CAP) {
-    uint64_t* a = s_keys;
-    uint64_t* b = s_keys + RS_CAP;
-    int* cnt = (int*)(s_keys + 2 * RS_CAP);
-    __shared__ uint32_t s_mm[2];
+  {  // tile_start = exclusive scan of the per-tile pair counts
+    int* sc = (int*)(s_keys + 2 * RS_CAP);  // [ntiles + 1] + tmp
+    block_exclusive_scan(A.tile_count, sc, A.ntiles, sc + A.ntiles + 1);
+    if (t == 0)
+      for (int j = threadIdx.x; j <= A.ntiles; j += blockDim.x) A.tile_start[j] = sc[j];
     if (threadIdx.x == 0) {
+      s_start[0] = sc[t];
+      s_start[1] = sc[t + 1];
+      s_pos = 0;
       s_mm[0] = 0xFFFFFFFFu;
       s_mm[1] = 0u;
     }
     __syncthreads();
+  }
+  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  const int s = s_start[0], n = s_start[1] - s;
+  uint64_t* g = A.pairs + s;
+  {  // gather: one thread per staged segment (any order, the sort is total)
+    uint64_t* dst = n <= RS_CAP ? s_keys : g;
+    const int nseg = A.tile_cursor[t];
+    const int2* sg = A.seg + (int64_t)t * A.seg_stride;
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const uint64_t v = g[j];
-      a[j] = v;
-      const uint32_t c = (uint32_t)(v >> 32);
-      lo = min(lo, c);
-      hi = max(hi, c);
+    for (int j = threadIdx.x; j < nseg; j += blockDim.x) {
+      const int2 d = sg[j];
+      const int p = atomicAdd(&s_pos, d.y);
+      const uint64_t* src = A.stage + d.x;
+      int k = 0;
+      for (; k + 4 <= d.y; k += 4) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + k + u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dst[p + k + u] = v[u];
+          const uint32_t c = (uint32_t)(v[u] >> 32);
+          lo = min(lo, c);
+          hi = max(hi, c);
+        }
+      }
+      for (; k < d.y; ++k) {
+        const uint64_t v = __ldcg(src + k);
+        dst[p + k] = v;
+        const uint32_t c = (uint32_t)(v >> 32);
+        lo = min(lo, c);
+        hi = max(hi, c);
+      }
     }
     lo = __reduce_min_sync(0xffffffffu, lo);
     hi = __reduce_max_sync(0xffffffffu, hi);
@@ -419,6 +343,11 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* 
       atomicMax(&s_mm[1], hi);
     }
     __syncthreads();
+  }
+  if (n > 1 && n <= RS_CAP) {
+    uint64_t* a = s_keys;
+    uint64_t* b = s_keys + RS_CAP;
+    int* cnt = (int*)(s_keys + 2 * RS_CAP);
     const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
     const int bits = span ? 32 - __clz(span) : 0;
     // one bucket pass on the top 13 bits of the tile-relative coarse key
@@ -497,65 +426,49 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(uint64_t* pairs, const int* 
       }
       __syncthreads();
       r = b;
-      fix_coarse_ties(r, n, key);
+      fix_coarse_ties(r, n, A.key);
     } else {  // a heavily populated bucket: stable LSD radix passes
       const int shift = bits > 24 ? bits - 24 : 0;
       const int npass = (bits - shift + 7) / 8;  // 0..3
       r = block_radix_sort(a, b, cnt, n, cmin, shift, npass);
-      fix_coarse_ties(r, n, key, cmin, shift);
+      fix_coarse_ties(r, n, A.key, cmin, shift);
     }
     __syncthreads();
     for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = r[j];
+  } else if (n == 1) {
+    if (threadIdx.x == 0) g[0] = s_keys[0];
   } else if (n > RS_CAP) {
-    if (threadIdx.x == 0) atomicAdd(counters + GSPARC_CNT_BIGTILE, 1);
+    if (threadIdx.x == 0) atomicAdd(A.counters + GSPARC_CNT_BIGTILE, 1);
     bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
-    fix_coarse_ties(g, n, key);
+    fix_coarse_ties(g, n, A.key);
     __syncthreads();
-  }
-  if (pair_rec) {
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const uint32_t idx = (uint32_t)g[j];
-      const float4 a4 = __ldg(rec32 + 2 * idx), b4 = __ldg(rec32 + 2 * idx + 1);
-      pair_rec[2 * (size_t)(s + j)] = a4;
-      pair_rec[2 * (size_t)(s + j) + 1] = make_float4(b4.x, b4.y, __int_as_float((int)idx), 0.f);
-    }
   }
 }
 
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
-  BinArgs A;
-  A.key = (const uint64_t*)(frame + L.off_key);
-  A.rect = (const int4*)(frame + L.off_rect);
-  A.tile_count = (const int*)(frame + L.off_tile_count);
-  A.tile_cursor = (int*)(frame + L.off_tile_cursor);
-  A.tile_start = (int*)(frame + L.off_tile_start);
-  A.counters = (int*)(frame + L.off_counters);
+  SortArgs A;
   A.pairs = (uint64_t*)(frame + L.off_pairs);
-  A.capacity = L.pair_capacity;
-  A.n = L.n;
-  A.ntx = L.ntx;
+  A.tile_start = (int*)(frame + L.off_tile_start);
+  A.key = (const uint64_t*)(frame + L.off_key);
+  A.counters = (int*)(frame + L.off_counters);
+  A.tile_count = (const int*)(frame + L.off_tile_count);
+  A.tile_cursor = (const int*)(frame + L.off_tile_cursor);
+  A.seg = (const int2*)(frame + L.off_seg);
+  A.stage = (const uint64_t*)(frame + L.off_stage);
+  A.seg_stride = L.seg_stride;
   A.ntiles = L.ntiles;
-  if (cudaMemsetAsync(A.tile_cursor, 0, sizeof(int) * L.ntiles, st) != cudaSuccess)
-    return check_launch("bin memset");
-  int blocks = (int)((L.n + 255) / 256);
-  if (blocks < 1) blocks = 1;
-  size_t smem = sizeof(int) * (3 * (size_t)L.ntiles + 1 + 40);
-  k_bin<<<blocks, 256, smem, st>>>(A);
-  GS_TRY(check_launch("k_bin"));
-  const size_t smem_sort =
-      2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * (size_t)max(RS_W * 256 + 512, 2 * BK_N);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
-    attr_set = true;
+  const size_t cnt_ints = (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + 1 + RS_W + 1);
+  const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;
+  if (smem_sort > 227 * 1024) {
+    set_error("bin_tiles: %d tiles exceed the sort kernel's shared memory", L.ntiles);
+    return GSPARC_ERR_UNSUPPORTED;
   }
-  int idx_bits = 8;
-  while (idx_bits < 32 && ((int64_t)1 << idx_bits) < L.n) idx_bits += 8;
-  float4* pair_rec = nullptr;  // the f32 raster gathers rrec by index
-  k_tile_sort<<<L.ntiles, RS_T, smem_sort, st>>>(A.pairs, A.tile_start, A.key, A.counters,
-                                           (const float4*)(frame + L.off_rec32), pair_rec,
-                                           idx_bits);
+  static size_t attr_set = 0;
+  if (attr_set < smem_sort) {
+    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
+    attr_set = smem_sort;
+  }
+  k_tile_sort<<<L.ntiles, RS_T, smem_sort, st>>>(A);
   return check_launch("k_tile_sort");
 }
 

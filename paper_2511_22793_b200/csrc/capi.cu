@@ -137,13 +137,15 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
     o = align_up(o + bytes);
     return r;
   };
+  // counters, tile_count and tile_cursor are contiguous: gsparc_prepare
+  // zeroes them with one memset
   L.off_counters = take(sizeof(int) * GSPARC_NUM_COUNTERS);
+  L.off_tile_count = take(sizeof(int) * L.ntiles);
+  L.off_tile_cursor = take(sizeof(int) * L.ntiles);
   L.off_key = take(8 * nn);
   L.off_rec32 = take(32 * nn);
   L.off_rec64 = take(dtype == GSPARC_F64 ? 64 * nn : 0);
   L.off_rect = take(16 * nn);
-  L.off_tile_count = take(sizeof(int) * L.ntiles);
-  L.off_tile_cursor = take(sizeof(int) * L.ntiles);
   L.off_tile_start = take(sizeof(int) * (L.ntiles + 1));
   L.off_tile_stop = take(sizeof(int) * L.ntiles * 4);  // per sub-tile
   L.off_pairs = take(8 * pair_capacity);
@@ -171,6 +173,9 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   const int64_t det_chunks = channels >= 4 ? (channels + 3) / 4 : 1;
   L.off_det_gcoef = det ? take(esz * pair_capacity * 4 * channels) : 0;
   L.off_det_ggeo = det ? take(esz * pair_capacity * 4 * det_chunks * 6) : 0;
+  L.seg_stride = (nn + PREP_T - 1) / PREP_T;
+  L.off_stage = take(8 * pair_capacity);
+  L.off_seg = take(8 * (int64_t)L.ntiles * L.seg_stride);
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

@@ -21,6 +21,7 @@
 namespace gs {
 
 constexpr int TILE = 16;
+constexpr int PREP_T = 128;  // k_preprocess CTA size = Gaussians per staged segment set
 constexpr int TILE_PX = TILE * TILE;
 constexpr double NEAR_PLANE = 0.05;      // geometry.py:27
 constexpr double FAR_PLANE = 1000.0;     // geometry.py:28
@@ -98,6 +99,44 @@ template <typename R>
 struct AlphaOut {
   R alpha, raw, g, dx, dy;
 };
+
+// Block-wide exclusive scan of `in[0..n)` into `out[0..n]` (out[n] = total),
+// any n, blockDim multiple of 32.  Uses `tmp` of blockDim/32+1 ints.
+__device__ inline void block_exclusive_scan(const int* in, int* out, int n, int* tmp) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int beg = min(n, tid * per), end = min(n, beg + per);
+  int local = 0;
+  for (int k = beg; k < end; ++k) local += in[k];
+  // inclusive warp scan of `local`
+  int lane = tid & 31, warp = tid >> 5;
+  int v = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) tmp[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = nt >> 5;
+    int w = lane < nw ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += u;
+    }
+    if (lane < nw) tmp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  int run = v - local + (warp > 0 ? tmp[warp - 1] : 0);
+  for (int k = beg; k < end; ++k) {
+    out[k] = run;
+    run += in[k];
+  }
+  if (tid == nt - 1) out[n] = run;
+  __syncthreads();
+}
 
 // exp for the f32 raster: 2^(x log2 e) with the product error carried
 // (t + e = x log2 e exactly to ~2^-48) and one ex2.approx; ~2 ulp, branch

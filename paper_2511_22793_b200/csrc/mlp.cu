@@ -213,7 +213,9 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
   } else if (A.C % 4 == 0 && A.C >= 16 && A.C <= 128 && A.H == 16 && A.I == 5) {
     int64_t threads = cloud.n * 32;
     int64_t blocks = (threads + 255) / 256;
-    if (live_only && blocks > 148 * 16) blocks = 148 * 16;  // grid-stride over the list
+    // live list: one wave (2 CTAs per SM), grid-stride over the list; most
+    // renders have fewer live Gaussians than resident warps
+    if (live_only && blocks > 148 * 2) blocks = 148 * 2;
     k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
   } else {
     int64_t threads = cloud.n * B;

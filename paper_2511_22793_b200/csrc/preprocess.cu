@@ -20,8 +20,14 @@ struct PrepArgs {
   double* rec64;
   float4* rrec;
   int4* rect;
+  int* live;
   int* counters;
   int* tile_count;
+  int* tile_cursor;
+  uint64_t* stage;
+  int2* seg;
+  int64_t capacity;
+  int seg_stride;
 };
 
 __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, double b0, double b1,
@@ -31,15 +37,25 @@ __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, doub
 
 __device__ __forceinline__ double np_floor_div16(double v) { return floor(v / 16.0); }
 
-__global__ void __launch_bounds__(128) k_preprocess(PrepArgs A) {
-  extern __shared__ int s_tiles[];  // per-CTA tile histogram
+// Tile binning is fused in (the counting-sort digit of rasterizer.py:115-145's
+// per-tile lists): every CTA histograms its Gaussians' tile rectangles,
+// reserves one contiguous stage range for all of them, registers one
+// segment {offset, length} per touched tile and scatters its packed pairs
+// (coarse depth << 32 | index).  Order inside a tile is irrelevant: K3 sorts
+// each tile's gathered segments by the full key.
+__global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
+  extern __shared__ int s_tiles[];  // per-CTA tile histogram [ntiles], offsets [ntiles+1], tmp
   const int ntiles = A.gc.ntx * A.gc.nty;
+  int* s_off = s_tiles + ntiles;
+  int* s_tmp = s_off + ntiles + 1;
+  __shared__ int s_base;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
   __syncthreads();
 
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool kept_out = false;
-  int pairs_out = 0;
+  uint64_t packed = 0;
+  int ry0 = 0, ry1 = -1, ra0 = 0, ra1 = -1, rb0 = 0, rb1 = -1;
   if (i < A.cloud.n) {
     const double* P = A.cloud.positions + 3 * i;
     const double* W = A.pose.W;
@@ -226,6 +242,7 @@ __global__ void __launch_bounds__(128) k_preprocess(PrepArgs A) {
       r[6] = theta;
       r[7] = phi;
     }
+    A.live[i] = 0;  // K4 pass A flags the Gaussians with a contribution
     A.rect[i] = make_int4(y0 | (y1 << 16), (a0 & 0xffff) | (a1 << 16), (b0 & 0xffff) | (b1 << 16),
                           npairs);
     if (keep) {
@@ -235,20 +252,53 @@ __global__ void __launch_bounds__(128) k_preprocess(PrepArgs A) {
       }
     }
     kept_out = keep;
-    pairs_out = npairs;
+    packed = ((uint64_t)(uint32_t)((k - DEPTH_KEY_BASE) >> COARSE_SHIFT) << 32) | (uint32_t)i;
+    ry0 = y0;
+    ry1 = y1;
+    ra0 = a0;
+    ra1 = a1;
+    rb0 = b0;
+    rb1 = b1;
   }
   {
     unsigned kept_warp = __reduce_add_sync(0xffffffffu, kept_out ? 1u : 0u);
-    unsigned pairs_warp = __reduce_add_sync(0xffffffffu, (unsigned)pairs_out);
-    if ((threadIdx.x & 31) == 0) {
-      if (kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
-      if (pairs_warp) atomicAdd(A.counters + GSPARC_CNT_PAIRS, (int)pairs_warp);
-    }
+    if ((threadIdx.x & 31) == 0 && kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
   }
   __syncthreads();
+  block_exclusive_scan(s_tiles, s_off, ntiles, s_tmp);  // ends with a barrier
+  const int total = s_off[ntiles];
+  if (threadIdx.x == 0) {
+    const int base = total ? atomicAdd(A.counters + GSPARC_CNT_PAIRS, total) : 0;
+    s_base = base;
+    if ((int64_t)base + total > A.capacity) A.counters[GSPARC_CNT_OVERFLOW] = 1;
+  }
+  __syncthreads();
+  const int base = s_base;
+  const bool fits = (int64_t)base + total <= A.capacity;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    int v = s_tiles[t];
-    if (v) atomicAdd(A.tile_count + t, v);
+    const int v = s_tiles[t];
+    if (v) {
+      atomicAdd(A.tile_count + t, v);
+      if (fits) {
+        const int slot = atomicAdd(A.tile_cursor + t, 1);
+        A.seg[(int64_t)t * A.seg_stride + slot] = make_int2(base + s_off[t], v);
+      }
+    }
+    s_off[t] += base;
+  }
+  __syncthreads();
+  if (kept_out && fits) {
+    const int ntx = A.gc.ntx;
+    for (int ty = ry0; ty <= ry1; ++ty) {
+      for (int tx = ra0; tx <= ra1; ++tx) {
+        const int t = ty * ntx + tx;
+        A.stage[atomicAdd(s_off + t, 1)] = packed;
+      }
+      for (int tx = rb0; tx <= rb1; ++tx) {
+        const int t = ty * ntx + tx;
+        A.stage[atomicAdd(s_off + t, 1)] = packed;
+      }
+    }
   }
 }
 
@@ -266,14 +316,28 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.rect = (int4*)(frame + L.off_rect);
   A.counters = (int*)(frame + L.off_counters);
   A.tile_count = (int*)(frame + L.off_tile_count);
-  if (cudaMemsetAsync(frame + L.off_counters, 0, GSPARC_NUM_COUNTERS * sizeof(int), st) !=
-          cudaSuccess ||
-      cudaMemsetAsync(frame + L.off_tile_count, 0, sizeof(int) * L.ntiles, st) != cudaSuccess)
+  A.tile_cursor = (int*)(frame + L.off_tile_cursor);
+  A.live = (int*)(frame + L.off_live);
+  A.stage = (uint64_t*)(frame + L.off_stage);
+  A.seg = (int2*)(frame + L.off_seg);
+  A.capacity = L.pair_capacity;
+  A.seg_stride = (int)L.seg_stride;
+  // counters | tile_count | tile_cursor are laid out back to back
+  const int64_t zero_end = L.off_tile_cursor + (int64_t)sizeof(int) * L.ntiles;
+  if (L.off_tile_count < L.off_counters || L.off_tile_cursor < L.off_tile_count) {
+    set_error("preprocess: unexpected frame layout");
+    return GSPARC_ERR_ARG;
+  }
+  if (cudaMemsetAsync(frame + L.off_counters, 0, zero_end - L.off_counters, st) != cudaSuccess)
     return check_launch("preprocess memset");
   if (cloud.n > 0) {
-    int blocks = (int)((cloud.n + 127) / 128);
-    size_t smem = sizeof(int) * (size_t)L.ntiles;
-    k_preprocess<<<blocks, 128, smem, st>>>(A);
+    const int blocks = (int)((cloud.n + PREP_T - 1) / PREP_T);
+    if (blocks > L.seg_stride) {
+      set_error("preprocess: frame planned for fewer Gaussians");
+      return GSPARC_ERR_ARG;
+    }
+    const size_t smem = sizeof(int) * (2 * (size_t)L.ntiles + 1 + PREP_T / 32 + 1);
+    k_preprocess<<<blocks, PREP_T, smem, st>>>(A);
   }
   return check_launch("k_preprocess");
 }

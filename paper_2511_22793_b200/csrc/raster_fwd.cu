@@ -346,10 +346,6 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
   }
   // f32 frames: one pixel per lane, tcgen05 accumulation (raster_px.cu)
   if (L.dtype == GSPARC_F32) return launch_raster_px(L, frame, n_tx, C, t_eps, pass, img, st);
-  if (pass != 2) {
-    if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
-      return check_launch("raster live memset");
-  }
   if (L.dtype == GSPARC_F64) {
     if (pass == 1) {
       launch_cfg<double, 64, 1, true, false, true>(A, 1, st);

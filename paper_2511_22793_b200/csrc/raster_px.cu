@@ -819,8 +819,6 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
     gsparc_dbg_ptr = dbga;
   }
   if (pass != 2) {
-    if (cudaMemsetAsync(A.live, 0, sizeof(int) * L.n, st) != cudaSuccess)
-      return check_launch("raster live memset");
     const int grid = L.ntiles * 2;
     if (pass == 0 && Cp <= 4) {
       switch (Cp) {

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.gsparc_abi_version() == 2
+    assert L.gsparc_abi_version() == 3
 
 
 def test_plan_frame_layout(L):
@@ -56,6 +56,13 @@ def test_plan_frame_layout(L):
     # chunk slots bound the CTA chunk lists of any pair layout
     assert lay.ch_slots >= 2 * (200000 + 31 * 138) // 32
     assert lay.off_ch_T + 4 * 128 * lay.ch_slots <= lay.total_bytes
+    # staged segments: one slot per (preprocess CTA of 128 Gaussians, tile)
+    assert lay.seg_stride == 4096 // 128
+    assert lay.off_stage % 256 == 0 and lay.off_seg % 256 == 0
+    assert lay.off_stage + 8 * 200000 <= lay.off_seg
+    assert lay.off_seg + 8 * 138 * lay.seg_stride <= lay.total_bytes
+    # counters, tile_count, tile_cursor are contiguous (one memset)
+    assert lay.off_counters < lay.off_tile_count < lay.off_tile_cursor < lay.off_key
 
 
 def test_plan_frame_rejects_bad_args(L):
