@@ -196,7 +196,8 @@ constexpr int RS_E = 8;
 constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
 constexpr int BK_BITS = 13;          // bucket pass: top 13 bits of the key
 constexpr int BK_N = 1 << BK_BITS;
-constexpr int BK_BIG = 64;           // larger buckets -> LSD radix fallback
+constexpr int BK_BIG = 64;
+constexpr int SEG_MAX = 4096;        // staged segments per tile gathered in parallel           // larger buckets -> LSD radix fallback
 
 __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n,
                                       uint32_t cmin, int shift, int npass) {
@@ -289,61 +290,100 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   __shared__ int s_pos;
   __shared__ uint32_t s_mm[2];
   const int t = blockIdx.x;
-  {  // tile_start = exclusive scan of the per-tile pair counts
-    int* sc = (int*)(s_keys + 2 * RS_CAP);  // [ntiles + 1] + tmp
-    block_exclusive_scan(A.tile_count, sc, A.ntiles, sc + A.ntiles + 1);
-    if (t == 0)
-      for (int j = threadIdx.x; j <= A.ntiles; j += blockDim.x) A.tile_start[j] = sc[j];
-    if (threadIdx.x == 0) {
-      s_start[0] = sc[t];
-      s_start[1] = sc[t + 1];
-      s_pos = 0;
-      s_mm[0] = 0xFFFFFFFFu;
-      s_mm[1] = 0u;
+  int* sc = (int*)(s_keys + 2 * RS_CAP);  // tile scan [ntiles + 1] + tmp [RS_W + 1]
+  int* s_soff = sc + A.ntiles + RS_W + 2;  // staged segments: offset, length, prefix
+  int* s_slen = s_soff + SEG_MAX;
+  int* s_spre = s_slen + SEG_MAX;
+  // the segment descriptors are loaded first so their latency overlaps the
+  // tile scan
+  const int nseg = __ldcg(A.tile_cursor + t);
+  const int2* sg = A.seg + (int64_t)t * A.seg_stride;
+  const bool seg_fast = nseg <= SEG_MAX;
+  int2 dsc[SEG_MAX / RS_T];
+  if (seg_fast) {
+#pragma unroll
+    for (int k = 0; k < SEG_MAX / RS_T; ++k) {
+      const int j = threadIdx.x + k * RS_T;
+      dsc[k] = j < nseg ? __ldcg(sg + j) : make_int2(0, 0);
     }
-    __syncthreads();
   }
+  // tile_start = exclusive scan of the per-tile pair counts
+  block_exclusive_scan(A.tile_count, sc, A.ntiles, sc + A.ntiles + 1);
+  if (t == 0)
+    for (int j = threadIdx.x; j <= A.ntiles; j += blockDim.x) A.tile_start[j] = sc[j];
+  if (threadIdx.x == 0) {
+    s_start[0] = sc[t];
+    s_start[1] = sc[t + 1];
+    s_pos = 0;
+    s_mm[0] = 0xFFFFFFFFu;
+    s_mm[1] = 0u;
+  }
+  if (seg_fast) {
+#pragma unroll
+    for (int k = 0; k < SEG_MAX / RS_T; ++k) {
+      const int j = threadIdx.x + k * RS_T;
+      if (j < nseg) {
+        s_soff[j] = dsc[k].x;
+        s_slen[j] = dsc[k].y;
+      }
+    }
+  }
+  __syncthreads();
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const int s = s_start[0], n = s_start[1] - s;
   uint64_t* g = A.pairs + s;
-  {  // gather: one thread per staged segment (any order, the sort is total)
-    uint64_t* dst = n <= RS_CAP ? s_keys : g;
-    const int nseg = A.tile_cursor[t];
-    const int2* sg = A.seg + (int64_t)t * A.seg_stride;
-    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-    for (int j = threadIdx.x; j < nseg; j += blockDim.x) {
-      const int2 d = sg[j];
-      const int p = atomicAdd(&s_pos, d.y);
-      const uint64_t* src = A.stage + d.x;
-      int k = 0;
-      for (; k + 4 <= d.y; k += 4) {
-        uint64_t v[4];
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  if (seg_fast && n <= RS_CAP) {
+    // every entry finds its segment by binary search over the length
+    // prefix; all loads of a thread are in flight together
+    block_exclusive_scan(s_slen, s_spre, nseg, sc + A.ntiles + 1);
+    uint64_t v[RS_E];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + k + u);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          dst[p + k + u] = v[u];
-          const uint32_t c = (uint32_t)(v[u] >> 32);
-          lo = min(lo, c);
-          hi = max(hi, c);
+    for (int e = 0; e < RS_E; ++e) {
+      const int j = threadIdx.x + e * RS_T;
+      v[e] = 0;
+      if (j < n) {
+        int l = 0, r = nseg - 1;  // last segment with prefix <= j
+        while (l < r) {
+          const int m = (l + r + 1) >> 1;
+          if (s_spre[m] <= j) l = m;
+          else r = m - 1;
         }
+        v[e] = __ldcg(A.stage + s_soff[l] + (j - s_spre[l]));
       }
-      for (; k < d.y; ++k) {
-        const uint64_t v = __ldcg(src + k);
-        dst[p + k] = v;
-        const uint32_t c = (uint32_t)(v >> 32);
+    }
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int j = threadIdx.x + e * RS_T;
+      if (j < n) {
+        s_keys[j] = v[e];
+        const uint32_t c = (uint32_t)(v[e] >> 32);
         lo = min(lo, c);
         hi = max(hi, c);
       }
     }
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(&s_mm[0], lo);
-      atomicMax(&s_mm[1], hi);
+  } else {  // one thread per staged segment (any order, the sort is total)
+    uint64_t* dst = n <= RS_CAP ? s_keys : g;
+    for (int j = threadIdx.x; j < nseg; j += blockDim.x) {
+      const int2 d = __ldcg(sg + j);
+      const int p = atomicAdd(&s_pos, d.y);
+      const uint64_t* src = A.stage + d.x;
+      for (int k = 0; k < d.y; ++k) {
+        const uint64_t x = __ldcg(src + k);
+        dst[p + k] = x;
+        const uint32_t c = (uint32_t)(x >> 32);
+        lo = min(lo, c);
+        hi = max(hi, c);
+      }
     }
-    __syncthreads();
   }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&s_mm[0], lo);
+    atomicMax(&s_mm[1], hi);
+  }
+  __syncthreads();
   if (n > 1 && n <= RS_CAP) {
     uint64_t* a = s_keys;
     uint64_t* b = s_keys + RS_CAP;
@@ -457,7 +497,8 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.stage = (const uint64_t*)(frame + L.off_stage);
   A.seg_stride = L.seg_stride;
   A.ntiles = L.ntiles;
-  const size_t cnt_ints = (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + 1 + RS_W + 1);
+  const size_t cnt_ints =
+      (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + RS_W + 2 + 3 * SEG_MAX + 1);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;
   if (smem_sort > 227 * 1024) {
     set_error("bin_tiles: %d tiles exceed the sort kernel's shared memory", L.ntiles);
