@@ -143,6 +143,14 @@ typedef struct gsparc_frame_layout {
   int64_t off_seg;        /* i32  [ntiles,seg_stride,2] staged segments
                              {stage offset, length} per tile              */
   int64_t seg_stride;     /* segment slots per tile (preprocess CTAs)     */
+  int64_t off_pxw;        /* f32  [2*ntiles,pxw_chunks,8,128,4] per-pixel
+                             blending weights T*alpha (entry quad, pixel,
+                             4 entries) of the first pxw_chunks chunks of
+                             every half-tile CTA, written by the weights
+                             pass (f32 frames)                           */
+  int64_t pxw_chunks;     /* chunks per CTA with stored weights          */
+  int64_t off_ch_wm;      /* u32  [slots,4] per 32-pixel warp: entries of
+                             the chunk with an included contribution     */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

@@ -176,6 +176,9 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.seg_stride = (nn + PREP_T - 1) / PREP_T;
   L.off_stage = take(8 * pair_capacity);
   L.off_seg = take(8 * (int64_t)L.ntiles * L.seg_stride);
+  L.pxw_chunks = dtype == GSPARC_F32 ? PXW_CHUNKS : 0;
+  L.off_pxw = take(4 * 2 * (int64_t)L.ntiles * L.pxw_chunks * 128 * 32);
+  L.off_ch_wm = take(dtype == GSPARC_F32 ? 4 * 4 * L.ch_slots : 0);
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

@@ -27,6 +27,8 @@
 //   (Wh.ch + Wh.cl + Wl.ch) for fp32 accuracy, accumulator in TMEM.
 #include <cuda.h>
 #include <stdlib.h>
+
+#include <type_traits>
 #include <string.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 
 #include "common.cuh"
@@ -56,6 +58,9 @@ struct PxArgs {
   int* live_list;
   int* counters;
   float* img;
+  float4* pxw;    // [2*ntiles][wmax][8][128] weights of the first wmax chunks
+  uint32_t* ch_wm;  // [slots][4] per-warp included-entry mask
+  int wmax;
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
   float t_eps, wf, inv_w;
@@ -298,21 +303,29 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       if (n < 0) break;
       const long long tc0 = clock64();
       A.ch_T[(slot0 + c) * 128 + warp * 32 + lane] = T;  // checkpoint for pass B
+      // the pixel's 32 blending weights of this chunk, stored for pass B
+      // (coalesced: entry quad j of the CTA's 128 pixels is one 2 KB row)
+      const bool wst = !SC && c < A.wmax;
+      float4* wrow = A.pxw + ((int64_t)blockIdx.x * A.wmax + c) * 8 * 128 + warp * 32 + lane;
+      unsigned um = 0;
       if (!wdone) {
         unsigned actm = 0;
         float Tl = T;
+        float wq[PX_K];
 #pragma unroll
         for (int k = 0; k < PX_K; ++k) {
           const float4 r0 = s_ring[s][k][0], r1 = s_ring[s][k][1];
           const float a = fast_alpha(pcx, pcy, r0, r1, wf, inv_w);
           const bool act = Tl >= teps && a > 0.f;
+          const float wgt = act ? Tl * a : 0.f;
           if (SC) {
-            const float wgt = act ? Tl * a : 0.f;
             const float4 cf = *(const float4*)&s_cf[s][k][0];
             acc[0] = fmaf(wgt, cf.x, acc[0]);
             if (SC > 1) acc[1] = fmaf(wgt, cf.y, acc[1]);
             if (SC > 2) acc[2] = fmaf(wgt, cf.z, acc[2]);
             if (SC > 3) acc[3] = fmaf(wgt, cf.w, acc[3]);
+          } else {
+            wq[k] = wgt;
           }
           Tl = act ? Tl * (1.f - a) : Tl;
           actm |= act ? (1u << k) : 0u;
@@ -322,7 +335,12 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
           cnt += __popc(actm);
           last = __float_as_int(s_ring[s][31 - __clz(actm)][1].z) + 1;
         }
-        const unsigned um = __reduce_or_sync(0xffffffffu, actm);
+        um = __reduce_or_sync(0xffffffffu, actm);
+        if (!SC && wst && um) {
+#pragma unroll
+          for (int j = 0; j < PX_K / 4; ++j)
+            wrow[j * 128] = make_float4(wq[4 * j], wq[4 * j + 1], wq[4 * j + 2], wq[4 * j + 3]);
+        }
         if (um) {
           lastch = c + 1;
           if (lane == 0) atomicOr(A.ch_used + slot0 + c, um);
@@ -330,6 +348,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         wdone = !__any_sync(0xffffffffu, T >= teps);
         if (wdone && lane == 0) atomicAdd(&s_ndone, 1);
       }
+      if (wst && lane == 0) A.ch_wm[(slot0 + c) * 4 + warp] = um;  // 0: no weights stored
       tcc += clock64() - tc0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[s]);
@@ -465,6 +484,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   unsigned char* sB = sm;  // [2 stages][hi|lo][8 entry groups][NA atoms][4 rows][128 B]
   __shared__ __align__(16) float4 s_rec[8][2 * PX_K];  // per weight warp
+  __shared__ int s_cidx[8][PX_K];                       // source index of K column
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_done;
   __shared__ uint32_t s_tmem;
   __shared__ int s_next;  // next chunk whose MMAs may be issued (order token)
@@ -523,52 +543,81 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
     float nT = 0.f;
     uint32_t nused = 0;
-    auto prefetch = [&](int c) {
+    int nidx = -1;
+    uint32_t nwm = 0;
+    int* cidx = s_cidx[warp];
+    // chunks c < wmax: pass A stored the pixels' weights (pxw); later chunks
+    // recompute them from the T checkpoint and the entry records
+    auto prefetch = [&](int c, bool wp) {
       if (c < nch) {
         const int64_t slot = slot0 + c;
-        n0 = A.ch_rec[2 * (slot * PX_K + lane)];
-        n1 = A.ch_rec[2 * (slot * PX_K + lane) + 1];
-        nT = A.ch_T[slot * 128 + q * 32 + lane];
         nused = A.ch_used[slot];
+        if (wp) {
+          nidx = (int)A.ch_idx[slot * PX_K + lane];
+          nwm = A.ch_wm[slot * 4 + q];
+        } else {
+          n0 = A.ch_rec[2 * (slot * PX_K + lane)];
+          n1 = A.ch_rec[2 * (slot * PX_K + lane) + 1];
+          nT = A.ch_T[slot * 128 + q * 32 + lane];
+        }
       }
     };
-    prefetch(gq);
     long long tw = 0, tc = 0;
-    for (int c = gq; c < nch; c += 2) {
+    auto chunk = [&](auto wp_tag, int c) {
+      constexpr bool wp = decltype(wp_tag)::value;
       const int k = c >> 1;
       float T = nT;
       const uint32_t used = nused;
-      __syncwarp();  // previous chunk's readers are done with rs
-      // compact the chunk's used entries (pass-A mask: at least one pixel of
-      // the CTA includes them) to the front, in list order.  Skipping an
-      // unused entry is exact: every pixel that is still live sees alpha = 0
-      // there.  The K order of the MMA is free as long as A columns and B
-      // rows agree, so column j is the j-th used entry; the rest are zero.
-      const int nu = __popc(used);
-      {
+      __syncwarp();  // previous chunk's readers are done with rs / cidx
+      // K column j of the chunk's MMA and the coef rows to load (mask lm):
+      //   stored weights: column j = entry j (list order); entries no pixel
+      //     of the CTA includes have zero weight everywhere, their B rows keep
+      //     stale finite data and are not loaded;
+      //   recomputed: the used entries compacted to the front (skipping an
+      //     unused entry is exact: every live pixel sees alpha = 0 there),
+      //     padding slots get zero records.
+      int nu;
+      uint32_t lm;
+      if (wp) {
+        cidx[lane] = nidx;
+        nu = PX_K;
+        lm = used;
+      } else {
+        nu = __popc(used);
+        lm = nu >= 32 ? 0xffffffffu : (1u << nu) - 1u;
         if (lane >= nu) {  // padding slots: zero opacity, alpha = 0
           rs[2 * lane] = make_float4(0.f, 0.f, 0.f, 0.f);
           rs[2 * lane + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+          cidx[lane] = -1;
         }
         if ((used >> lane) & 1u) {  // used entries, in list order
           const int slot = __popc(used & ((1u << lane) - 1u));
           rs[2 * slot] = n0;
           rs[2 * slot + 1] = n1;
+          cidx[slot] = __float_as_int(n1.w);
         }
       }
-      prefetch(c + 2);
+      float4 wr[PX_K / 4];
+      if (wp) {  // this pixel's stored weights (none stored: all zero)
+        const uint32_t wm = nwm;
+        const float4* src = A.pxw + ((int64_t)blockIdx.x * A.wmax + c) * 8 * 128 + q * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < PX_K / 4; ++j)
+          wr[j] = wm ? __ldcg(src + j * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (!wp || c + 2 < A.wmax) prefetch(c + 2, wp);
       __syncwarp();
-      // coef rows of the used entries, issued now and consumed after the
-      // alpha math: piece p = gt + 128 u of the 32 x PPR (entry, 16 B piece)
-      // grid; entry e is uniform per warp for PPR >= 32
+      // coef rows of the loaded columns, issued now and consumed after the
+      // weights: piece p = gt + 128 u of the 32 x PPR (column, 16 B piece)
+      // grid; the column is uniform per warp for PPR >= 32
       float4 cv[CF::NPF];
 #pragma unroll
       for (int u = 0; u < CF::NPF; ++u) {
         const int p = gt + 128 * u;
         const int e = p / CF::PPR, jj = p - e * CF::PPR;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < nu && jj < ppr) {
-          const int idx = __float_as_int(rs[2 * e + 1].w);
+        if (e < PX_K && ((lm >> e) & 1u) && jj < ppr) {
+          const int idx = cidx[e];
           if (idx >= 0) {
             const float* row = A.coef + (int64_t)idx * A.Cp + col0 + 4 * jj;
             if (vec) {
@@ -586,18 +635,28 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       }
       const long long t0 = clock64();
       float wv[PX_K];
+      if (wp) {
 #pragma unroll
-      for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
-      if (__any_sync(0xffffffffu, T >= teps)) {
+        for (int j = 0; j < PX_K / 4; ++j) {
+          wv[4 * j] = wr[j].x;
+          wv[4 * j + 1] = wr[j].y;
+          wv[4 * j + 2] = wr[j].z;
+          wv[4 * j + 3] = wr[j].w;
+        }
+      } else {
 #pragma unroll
-        for (int e0 = 0; e0 < PX_K; e0 += 8) {
-          if (e0 >= nu) break;  // uniform: groups of 8 keep the ILP
+        for (int e = 0; e < PX_K; ++e) wv[e] = 0.f;
+        if (__any_sync(0xffffffffu, T >= teps)) {
 #pragma unroll
-          for (int e = e0; e < e0 + 8; ++e) {
-            const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
-            const bool act = T >= teps && a > 0.f;
-            wv[e] = act ? T * a : 0.f;
-            T = act ? T * (1.f - a) : T;
+          for (int e0 = 0; e0 < PX_K; e0 += 8) {
+            if (e0 >= nu) break;  // uniform: groups of 8 keep the ILP
+#pragma unroll
+            for (int e = e0; e < e0 + 8; ++e) {
+              const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
+              const bool act = T >= teps && a > 0.f;
+              wv[e] = act ? T * a : 0.f;
+              T = act ? T * (1.f - a) : T;
+            }
           }
         }
       }
@@ -619,12 +678,12 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         tmem_st16(a_hi + 16 * hh, hi);
         tmem_st16(a_lo + 16 * hh, lo);
       }
-      // coef hi/lo planes of the used rows (rows of unused entries untouched)
+      // coef hi/lo planes of the loaded rows (other rows untouched)
 #pragma unroll
       for (int u = 0; u < CF::NPF; ++u) {
         const int p = gt + 128 * u;
         const int e = p / CF::PPR, jj = p - e * CF::PPR;
-        if (e < nu && jj < ppr) {
+        if (e < PX_K && ((lm >> e) & 1u) && jj < ppr) {
           const float4 x = cv[u];
           float4 h;
           h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -675,7 +734,14 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         *(volatile int*)&s_next = c + 1;
       }
       __syncwarp();
-    }
+    };
+    // stored-weight chunks, then (beyond wmax) recomputed ones
+    const int nw = min(nch, A.wmax);
+    int c = gq;
+    if (c < nw) prefetch(c, true);
+    for (; c < nw; c += 2) chunk(std::integral_constant<bool, true>(), c);
+    if (c < nch) prefetch(c, false);
+    for (; c < nch; c += 2) chunk(std::integral_constant<bool, false>(), c);
     if (A.dbg && lane == 0 && q == 0) {
       A.dbg[blockIdx.x * 16 + 6 + gq] = tw;
       A.dbg[blockIdx.x * 16 + 8 + gq] = tc;
@@ -791,6 +857,9 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.live_list = (int*)(frame + L.off_live_list);
   A.counters = (int*)(frame + L.off_counters);
   A.img = (float*)img;
+  A.pxw = (float4*)(frame + L.off_pxw);
+  A.ch_wm = (uint32_t*)(frame + L.off_ch_wm);
+  A.wmax = (int)L.pxw_chunks;
   A.Cp = (int64_t)n_tx * C;
   A.n = L.n;
   A.C = C;
