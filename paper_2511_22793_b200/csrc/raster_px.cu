@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_done;
   __shared__ uint32_t s_tmem;
   __shared__ int s_next;  // next chunk whose MMAs may be issued (order token)
+  __shared__ int s_acc;   // accumulator initialised (an MMA was issued)
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const long long t_start = clock64();
@@ -504,6 +505,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     }
     mbar_init(&s_done, 1);
     s_next = 0;
+    s_acc = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -710,9 +712,13 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ma_hi = tmem + CF::A_COL0 + 64 * gq, ma_lo = ma_hi + 32;
         const uint32_t mb_hi = smem_u32(bhi), mb_lo = mb_hi + CF::PLANE;
+        // K-steps whose 8 columns carry no coef row are all-zero in A: skip
+        // them (the first MMA issued initialises the accumulator)
 #pragma unroll
         for (int ks = 0; ks < PX_K / 8; ++ks) {
-          const uint32_t acc0 = (c > 0 || ks > 0) ? 1u : 0u;
+          if (((lm >> (8 * ks)) & 0xFFu) == 0u) continue;
+          const uint32_t acc0 = s_acc ? 1u : 0u;
+          s_acc = 1;
           const uint32_t ko = ks * CF::NA * 1024;  // 8 entries = 2 atom rows of K
           mma_tf32_ts(tmem, ma_hi + 8 * ks, umma_desc_mn_b32(mb_hi + ko, CF::NA * 512), idesc,
                       acc0);

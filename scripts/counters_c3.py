@@ -27,3 +27,22 @@ for lazy in (True, False):
         R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=lazy)
     e1.record(); torch.cuda.synchronize()
     print("lazy", lazy, "ms/render (eager launches)", e0.elapsed_time(e1) / 20)
+# used-entry statistics of the pass-B chunks (popcount of ch_used)
+img, frame = R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=True)
+torch.cuda.synchronize()
+Ly = frame.layout
+ts = frame.view("tile_start", torch.int32, (Ly.ntiles + 1,)).cpu().numpy().astype(np.int64)
+chn = frame.view("ch_n", torch.int32, (2 * Ly.ntiles,)).cpu().numpy()
+used = frame.view("ch_used", torch.int32, (int(Ly.ch_slots),)).cpu().numpy().view(np.uint32)
+pops, ksteps = [], []
+for cta in range(2 * Ly.ntiles):
+    t, h = cta >> 1, cta & 1
+    s, ln = ts[t], ts[t + 1] - ts[t]
+    slot0 = 2 * ((s + 31 * t) >> 5) + h * ((ln + 31) >> 5)
+    for c in range(chn[cta]):
+        u = int(used[slot0 + c])
+        pops.append(bin(u).count("1"))
+        ksteps.append(sum(1 for k in range(4) if (u >> (8 * k)) & 0xFF))
+pops, ksteps = np.array(pops), np.array(ksteps)
+print("chunks", len(pops), "used entries/chunk mean", pops.mean(), "K-steps mean", ksteps.mean(),
+      "compacted K-steps mean", np.ceil(pops / 8).mean())
