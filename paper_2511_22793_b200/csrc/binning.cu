@@ -14,10 +14,14 @@
 //     truncation (bits(depth) - bits(0.05)) >> 24; runs that tie on it are
 //     re-ordered by the full f64 bit pattern, so the final order is exactly
 //     np.lexsort((idx, depth)) restricted to the tile.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace gs {
+
+extern long long* gsparc_dbg_ptr;
 
 struct SortArgs {
   uint64_t* pairs;
@@ -30,6 +34,7 @@ struct SortArgs {
   const uint64_t* stage;
   int64_t seg_stride;
   int ntiles;
+  long long* dbg;  // experiments: per-CTA phase clocks (GSPARC_SORT_DBG)
 };
 
 // Ascending-only bitonic network on n elements (virtual +inf padding up to
@@ -196,8 +201,8 @@ constexpr int RS_E = 8;
 constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
 constexpr int BK_BITS = 13;          // bucket pass: top 13 bits of the key
 constexpr int BK_N = 1 << BK_BITS;
-constexpr int BK_BIG = 64;
-constexpr int SEG_MAX = 4096;        // staged segments per tile gathered in parallel           // larger buckets -> LSD radix fallback
+constexpr int BK_BIG = 64;           // larger buckets -> LSD radix fallback
+constexpr int SEG_MAX = 4096;        // staged segments per tile gathered in parallel
 
 __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n,
                                       uint32_t cmin, int shift, int npass) {
@@ -285,6 +290,7 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
 // Gather each tile's staged segments, sort them by (coarse depth, index),
 // fix coarse ties by the full f64 key and write the tile's list.
 __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
+  const long long t_dbg0 = clock64();
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
   __shared__ int s_start[2];
   __shared__ int s_pos;
@@ -329,6 +335,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     }
   }
   __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 1] = clock64() - t_dbg0;
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const int s = s_start[0], n = s_start[1] - s;
   uint64_t* g = A.pairs + s;
@@ -343,12 +350,11 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       const int j = threadIdx.x + e * RS_T;
       v[e] = 0;
       if (j < n) {
-        int l = 0, r = nseg - 1;  // last segment with prefix <= j
-        while (l < r) {
-          const int m = (l + r + 1) >> 1;
-          if (s_spre[m] <= j) l = m;
-          else r = m - 1;
-        }
+        int l = 0;  // last segment with prefix <= j (fixed steps: the
+                    // searches of a thread's keys interleave)
+#pragma unroll
+        for (int step = SEG_MAX / 2; step >= 1; step >>= 1)
+          if (l + step < nseg && s_spre[l + step] <= j) l += step;
         v[e] = __ldcg(A.stage + s_soff[l] + (j - s_spre[l]));
       }
     }
@@ -384,6 +390,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     atomicMax(&s_mm[1], hi);
   }
   __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 2] = clock64() - t_dbg0;
   if (n > 1 && n <= RS_CAP) {
     uint64_t* a = s_keys;
     uint64_t* b = s_keys + RS_CAP;
@@ -392,8 +399,8 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     const int bits = span ? 32 - __clz(span) : 0;
     // one bucket pass on the top 13 bits of the tile-relative coarse key
     // (shared-memory atomics; order inside a bucket is fixed next), then
-    // every bucket is insertion-sorted by (coarse32, index) and runs tying
-    // on coarse32 are put in exact (f64 key, index) order
+    // every key is ranked by (coarse32, index) inside its bucket and runs
+    // tying on coarse32 are put in exact (f64 key, index) order
     const int bshift = bits > BK_BITS ? bits - BK_BITS : 0;
     int* bcnt = cnt;              // [BK_N]
     int* bcur = cnt + BK_N;       // [BK_N]
@@ -407,6 +414,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       if (c == BK_BIG) atomicMax(&s_bmax, c);
     }
     __syncthreads();
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 3] = clock64() - t_dbg0;
     uint64_t* r;
     if (s_bmax < BK_BIG) {
       // exclusive scan of the bucket counts (BK_N / blockDim per thread)
@@ -446,26 +454,29 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
         bcnt[threadIdx.x * PER + k] = st0;  // bucket start
       }
       __syncthreads();
+      if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 4] = clock64() - t_dbg0;
       for (int j = threadIdx.x; j < n; j += blockDim.x) {
         const uint64_t v = a[j];
         const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
         b[atomicAdd(bcur + bk, 1)] = v;
       }
       __syncthreads();
-      for (int bk = threadIdx.x; bk < BK_N; bk += blockDim.x) {
+      // every key's rank inside its bucket: one pass over the (small)
+      // bucket per key, all keys in parallel; written to a in sorted order
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const uint64_t v = b[j];
+        const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
         const int lo = bcnt[bk], hi = bcur[bk];
-        for (int p = lo + 1; p < hi; ++p) {  // insertion sort, buckets are small
-          const uint64_t v = b[p];
-          int q = p - 1;
-          while (q >= lo && b[q] > v) {
-            b[q + 1] = b[q];
-            --q;
-          }
-          b[q + 1] = v;
+        int rank = lo;
+        for (int i = lo; i < hi; ++i) {
+          const uint64_t u = b[i];
+          rank += (u < v) || (u == v && i < j);  // equal keys: seam duplicates
         }
+        a[rank] = v;
       }
       __syncthreads();
-      r = b;
+      if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 5] = clock64() - t_dbg0;
+      r = a;
       fix_coarse_ties(r, n, A.key);
     } else {  // a heavily populated bucket: stable LSD radix passes
       const int shift = bits > 24 ? bits - 24 : 0;
@@ -474,6 +485,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       fix_coarse_ties(r, n, A.key, cmin, shift);
     }
     __syncthreads();
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 7] = clock64() - t_dbg0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) g[j] = r[j];
   } else if (n == 1) {
     if (threadIdx.x == 0) g[0] = s_keys[0];
@@ -497,6 +509,14 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.stage = (const uint64_t*)(frame + L.off_stage);
   A.seg_stride = L.seg_stride;
   A.ntiles = L.ntiles;
+  A.dbg = nullptr;
+  if (getenv("GSPARC_SORT_DBG")) {  // experiments only
+    static long long* dbg = nullptr;
+    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * 4096);
+    cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * 4096, st);
+    A.dbg = dbg;
+    gsparc_dbg_ptr = dbg;
+  }
   const size_t cnt_ints =
       (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + RS_W + 2 + 3 * SEG_MAX + 1);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;

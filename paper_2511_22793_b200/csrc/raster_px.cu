@@ -754,9 +754,12 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     }
   }
 
-  // ---------------- epilogue: warps 0..3 own TMEM lanes 32q.. (= pixels)
-  if (warp < 4) {
-    const int q = warp;
+  // ---------------- epilogue: warp w reads TMEM lanes 32 (w % 4).. (= pixels),
+  // columns [0, NPH) for w < 4 and [NPH, NP) for the second group
+  if (warp < 8) {
+    constexpr int NPH = ((NP / 2 + 7) / 8) * 8;
+    const int q = warp & 3;
+    const int cbeg = warp < 4 ? 0 : NPH, cend = warp < 4 ? NPH : NP;
     const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
     const bool inside = px < A.w && py < A.h;
     if (nch > 0) {
@@ -767,7 +770,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = te0 - t_start;
     const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < NP; c0 += 8) {
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
       uint32_t v[8];
       if (nch > 0) {
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
