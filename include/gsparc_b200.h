@@ -30,6 +30,11 @@
  *                           (optimize.py:165-188)
  *   gsparc_adam_step        optimize.adam_step (optimize.py:234-259) with
  *                           optimize.position_lr (optimize.py:205-213)
+ *   gsparc_gt_spectrum      rfsim.ground_truth_spectrum (rfsim.py:75-99)
+ *                           + free_space_amplitude (rfsim.py:65-71),
+ *                           batched over TX
+ *   gsparc_rssi_energy      the energy sum of rfsim.rssi_from_spectrum
+ *                           (rfsim.py:227-243), batched over images
  */
 #ifndef GSPARC_B200_H
 #define GSPARC_B200_H
@@ -243,6 +248,32 @@ int gsparc_adam_step(double* positions, double* log_scales, double* rotations,
                      int32_t mlp_params, const float* grad_flat, float* m_flat,
                      float* v_flat, int64_t* step_dev, int32_t* counters_dev,
                      const gsparc_adam_config* cfg, void* stream);
+
+/* Point emitter of the multipath oracle (rfsim.py:29-38). */
+typedef struct gsparc_emitter {
+  double position[3];
+  double gain_re, gain_im;
+  double angular_spread; /* radians, > 0 */
+} gsparc_emitter;
+
+/* K9: |field| at every pixel for each TX (rfsim.ground_truth_spectrum),
+ * divided by `scale` when scale > 0.  emitters_dev: [n_emitters] device
+ * (1..256); rx: host double[3]; tx_dev: f64 [n_tx,3] device;
+ * out_dev: out_dtype [n_tx, height, width] device (row 0 = horizon). */
+int gsparc_gt_spectrum(const gsparc_emitter* emitters_dev, int32_t n_emitters,
+                       const double* rx, double wavelength,
+                       const double* tx_dev, int32_t n_tx, int32_t width,
+                       int32_t height, double scale, int32_t out_dtype,
+                       void* out_dev, void* stream);
+
+/* K10: energy_dev[b] = sum over the selected pixel indices sel_dev[0..n_sel)
+ * of re^2 (+ im^2 when channels == 2) of image b, in f64 (the sum of
+ * rfsim.rssi_from_spectrum before the 1/fraction and dB steps).
+ * img_dev: dtype [n_img, height, width, channels], channels 1 or 2. */
+int gsparc_rssi_energy(const void* img_dev, int32_t dtype, int32_t n_img,
+                       int32_t height, int32_t width, int32_t channels,
+                       const int64_t* sel_dev, int64_t n_sel,
+                       double* energy_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -903,3 +903,76 @@ def live_fraction(aux: Aux):
 
 def cpu_threads():
     return os.cpu_count() or 1
+
+
+# ------------------------------------------------- rfsim / RFSI wire format
+RSSI_FLOOR_DB = -100.0
+
+
+def free_space_amp(d, wavelength):
+    """rfsim.py:65-71."""
+    d = np.asarray(d, np.float64)
+    return (wavelength / (4.0 * np.pi * d)) * np.exp(-2j * np.pi * d / wavelength)
+
+
+def ground_truth(emitters, rx, wavelength, tx, w, h, scale=None):
+    """Closed-form multipath magnitude (rfsim.py:75-99).  emitters: list of
+    (position[3], complex gain, angular spread).  Returns (h, w) f64."""
+    tx = np.asarray(tx, np.float64).reshape(3)
+    rx = np.asarray(rx, np.float64).reshape(3)
+    uu, vv = np.meshgrid(np.arange(w), np.arange(h))
+    dirs = pixel_dir(uu.ravel(), vv.ravel(), w, h)
+    field = np.zeros(w * h, dtype=np.complex128)
+    for pos, gain, spread in emitters:
+        pos = np.asarray(pos, np.float64)
+        to_em = pos - rx
+        r_em = np.linalg.norm(to_em)
+        if r_em < 1e-9:
+            continue
+        path = np.linalg.norm(pos - tx) + r_em
+        amp = gain * free_space_amp(path, wavelength)
+        cosang = np.clip(dirs @ (to_em / r_em), -1.0, 1.0)
+        ang = np.arccos(cosang)
+        field += amp * np.exp(-ang * ang / (2.0 * spread ** 2))
+    mag = np.abs(field).reshape(h, w)
+    return mag / scale if scale is not None else mag
+
+
+def select_pixels(seed, w, h, fraction):
+    """The PCG64 pixel subset of rssi_from_spectrum (rfsim.py:215-218,230)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n_total = w * h
+    return rng.choice(n_total, size=int(np.ceil(fraction * n_total)),
+                      replace=False)
+
+
+def energy_db(energy, offset=0.0):
+    """rfsim.py:221-224."""
+    return RSSI_FLOOR_DB if energy <= 0.0 else 10.0 * np.log10(energy) + offset
+
+
+def rssi(img, fraction, seed, offset=0.0):
+    """rssi_from_spectrum (rfsim.py:227-243); img (h, w, c), c = 1 or 2."""
+    d = np.asarray(img, np.float64)
+    e = d[:, :, 0] ** 2 + d[:, :, 1] ** 2 if d.shape[2] == 2 else d[:, :, 0] ** 2
+    sel = select_pixels(seed, d.shape[1], d.shape[0], fraction)
+    return energy_db(float(e.reshape(-1)[sel].sum()) / fraction, offset)
+
+
+def write_rfsi(path, data):
+    """RFSI v1 writer (image.py:64-69)."""
+    d = np.asarray(data)
+    h, w, c = d.shape
+    with open(path, "wb") as f:
+        f.write(b"RFSI" + struct.pack("<4I", 1, w, h, c))
+        f.write(np.ascontiguousarray(d, "<f4").tobytes())
+
+
+def read_rfsi(path):
+    """RFSI v1 reader (image.py:72-86)."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    assert buf[:4] == b"RFSI"
+    ver, w, h, c = struct.unpack("<4I", buf[4:20])
+    assert ver == 1
+    return np.frombuffer(buf, "<f4", count=w * h * c, offset=20).reshape(h, w, c)

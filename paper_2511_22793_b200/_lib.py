@@ -56,6 +56,11 @@ class CLayout(ctypes.Structure):
                  ("off_pxw", c_i64), ("pxw_chunks", c_i64), ("off_ch_wm", c_i64)])
 
 
+class CEmitter(ctypes.Structure):
+    _fields_ = [("position", c_dbl * 3), ("gain_re", c_dbl), ("gain_im", c_dbl),
+                ("angular_spread", c_dbl)]
+
+
 class CAdamConfig(ctypes.Structure):
     _fields_ = [(k, c_dbl) for k in (
         "position_lr_init", "position_lr_final", "position_lr_delay_mult",
@@ -101,6 +106,10 @@ def lib():
         "gsparc_adam_step": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32,
                                      c_vp, c_vp, c_vp, c_vp, c_vp,
                                      P(CAdamConfig), c_vp]),
+        "gsparc_gt_spectrum": (c_i32, [c_vp, c_i32, P(c_dbl), c_dbl, c_vp, c_i32,
+                                       c_i32, c_i32, c_dbl, c_i32, c_vp, c_vp]),
+        "gsparc_rssi_energy": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                       c_vp, c_i64, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -119,7 +128,8 @@ def exported_symbols():
             "gsparc_prepare", "gsparc_bin_tiles", "gsparc_mlp_coef",
             "gsparc_raster_forward", "gsparc_render_forward",
             "gsparc_render_backward", "gsparc_loss_scratch_bytes",
-            "gsparc_loss_fwd_bwd", "gsparc_adam_step"]
+            "gsparc_loss_fwd_bwd", "gsparc_adam_step", "gsparc_gt_spectrum",
+            "gsparc_rssi_energy"]
 
 
 class GsparcError(RuntimeError):

@@ -306,4 +306,19 @@ int gsparc_adam_step(double* positions, double* log_scales, double* rotations,
                      (cudaStream_t)stream);
 }
 
+int gsparc_gt_spectrum(const gsparc_emitter* emitters_dev, int32_t n_emitters, const double* rx,
+                       double wavelength, const double* tx_dev, int32_t n_tx, int32_t width,
+                       int32_t height, double scale, int32_t out_dtype, void* out_dev,
+                       void* stream) {
+  return launch_gt_spectrum(emitters_dev, n_emitters, rx, wavelength, tx_dev, n_tx, width, height,
+                            scale, out_dtype, out_dev, (cudaStream_t)stream);
+}
+
+int gsparc_rssi_energy(const void* img_dev, int32_t dtype, int32_t n_img, int32_t height,
+                       int32_t width, int32_t channels, const int64_t* sel_dev, int64_t n_sel,
+                       double* energy_dev, void* stream) {
+  return launch_rssi_energy(img_dev, dtype, n_img, height, width, channels, sel_dev, n_sel,
+                            energy_dev, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -29,4 +29,10 @@ int launch_adam(double* pos, double* ls, double* rot, double* op, float* mlp, in
                 const float* g, float* m, float* v, int64_t* step, int* counters,
                 const gsparc_adam_config& cfg, cudaStream_t st);
 
+int launch_gt_spectrum(const gsparc_emitter* em_dev, int ne, const double* rx, double wavelength,
+                       const double* tx_dev, int B, int w, int h, double scale, int out_dtype,
+                       void* out, cudaStream_t st);
+int launch_rssi_energy(const void* img, int dtype, int B, int h, int w, int C, const int64_t* sel,
+                       int64_t nsel, double* energy, cudaStream_t st);
+
 }  // namespace gs

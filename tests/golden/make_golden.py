@@ -126,11 +126,54 @@ def dup_case():
     raise RuntimeError("no seam duplicate found")
 
 
+def rfsim_case():
+    """Ground truth, RSSI, RFSI bytes and a tiny gen_dataset from the real
+    rfsim / image modules (rfsim.py:65-256, image.py:64-86)."""
+    import tempfile
+    sc = rfsim.random_scene(11, 6)
+    txs = rfsim._sample_tx_positions(np.random.Generator(np.random.PCG64(7)),
+                                     4, [-4, 0, -4], [4, 2, 4], sc.rx_position,
+                                     1.0)
+    w, h = 40, 12
+    gt = np.stack([rfsim.ground_truth_spectrum(sc, t, w, h).data[:, :, 0]
+                   for t in txs])
+    gt_scaled = rfsim.ground_truth_spectrum(sc, txs[0], w, h, scale=2.5).data
+    em = np.array([[*e.position, e.gain.real, e.gain.imag, e.angular_spread]
+                   for e in sc.emitters])
+    rng = np.random.default_rng(5)
+    img2 = rng.normal(size=(h, w, 2)).astype(np.float32)
+    img1 = np.abs(rng.normal(size=(h, w, 1))).astype(np.float32)
+    rssi = np.array([
+        rfsim.rssi_from_spectrum(image.SpectrumImage(img2), 0.3, 5),
+        rfsim.rssi_from_spectrum(image.SpectrumImage(img2), 1.0, 2, 3.5),
+        rfsim.rssi_from_spectrum(image.SpectrumImage(img1), 0.05, 9),
+        rfsim.rssi_from_spectrum(image.SpectrumImage(np.zeros((h, w, 1))), 0.5, 1)])
+    sel = rfsim._select_pixels(np.random.Generator(np.random.PCG64(5)), w, h, 0.3)
+    with tempfile.TemporaryDirectory() as td:
+        image.save_rfsi(os.path.join(td, "x.rfsi"), image.SpectrumImage(img2))
+        rfsi_bytes = np.frombuffer(open(os.path.join(td, "x.rfsi"), "rb").read(),
+                                   np.uint8)
+        idx = rfsim.gen_dataset(3, 3, sc, 24, 8, td)
+        files = sorted(f for f in os.listdir(td) if f.startswith("sample_"))
+        ds = {f"ds_{f[:-5]}": np.frombuffer(open(os.path.join(td, f), "rb").read(),
+                                            np.uint8) for f in files}
+        index_txt = open(idx).read()
+        manifest_txt = open(os.path.join(td, "manifest.txt")).read()
+    save("rfsim", emitters=em, rx=sc.rx_position, wavelength=sc.wavelength,
+         txs=txs, w=w, h=h, gt=gt, gt_scaled=gt_scaled, img2=img2, img1=img1,
+         rssi=rssi, sel=sel, rfsi_bytes=rfsi_bytes, index_txt=np.array(index_txt),
+         manifest_txt=np.array(manifest_txt), **ds)
+
+
 def main():
+    if sys.argv[1:] == ["--only", "rfsim"]:
+        rfsim_case()
+        return
     if sys.argv[1:] == ["--only", "bwd_dup"]:
         dup_case()
         return
     dup_case()
+    rfsim_case()
     # --- known answers (tests/test_rasterizer.py:33-70)
     d = 2.0 * pixel_to_direction(18, 4, 36, 9)
     fwd_case("ka_single", single(d), [0.0, 0.0, 0.0], 36, 9)
