@@ -13,6 +13,6 @@ timeout 300 python bench.py --config c2 --steps 50 > gpurun_out/bench_c2.json 2>
 timeout 400 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(px|tile_sort|bin|preprocess|mlp)" -s 12 -c 6 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(px|tile_sort|bin|preprocess|mlp)" -s 10 -c 5 \
   -o gpurun_out/prof_c3 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/prof_c3.log 2>&1
 ls -la gpurun_out
