@@ -469,8 +469,18 @@ def roofline_entry(dom, stages, n, P, C, B, h, w, live, pairs, hbm):
         "raster_fused": pairs * 8 + n * 4 * B * C + 4 * h * w * B * C + h * w * 12,
     }[dom]
     achieved = per / (us * 1e-6) / 1e9
+    # DRAM bytes (read + write) of the same kernel per launch, from the
+    # committed ncu --set full capture of this config (null if none)
+    traffic = None
+    try:
+        tf = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                         "profiles", "r01", "ncu_traffic_c3.json")))
+        if n == 50000 and C == 104:
+            traffic = tf["per_launch_bytes"].get(dom)
+    except (OSError, ValueError, KeyError):
+        pass
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-            "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+            "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
             "algorithmic_bytes": per, "launch_us": us,
             "note": "raster stages are issue/latency-bound (alpha compositing "
                     "on CUDA cores), so their HBM fraction is low by nature; "
