@@ -110,7 +110,7 @@ typedef struct gsparc_frame_layout {
   int64_t off_rect;       /* i32  [n,4] tile rectangle + pair count     */
   int64_t off_counters;   /* i32  [16]                                  */
   int64_t off_tile_count; /* i32  [ntiles] pairs per tile               */
-  int64_t off_tile_cursor;/* i32  [ntiles] staged segments per tile     */
+  int64_t off_tile_cursor;/* i32  [ntiles] reserved (zeroed)             */
   int64_t off_tile_start; /* i32  [ntiles+1]                            */
   int64_t off_tile_stop;  /* i32  [ntiles*4] list prefix visited per sub-tile */
   int64_t off_pairs;      /* u64  [pair_capacity] per-tile sorted lists */
@@ -145,8 +145,9 @@ typedef struct gsparc_frame_layout {
   int64_t off_stage;      /* u64  [pair_capacity] unsorted pairs staged
                              by gsparc_prepare, one contiguous segment per
                              (preprocess CTA, tile)                       */
-  int64_t off_seg;        /* i32  [ntiles,seg_stride,2] staged segments
-                             {stage offset, length} per tile              */
+  int64_t off_seg;        /* i32  [ntiles,seg_stride,2] staged segment of
+                             preprocess CTA s for tile t: {stage offset,
+                             length}, length 0 when the CTA has none      */
   int64_t seg_stride;     /* segment slots per tile (preprocess CTAs)     */
   int64_t off_pxw;        /* f32  [2*ntiles,pxw_chunks,8,128,4] per-pixel
                              blending weights T*alpha (entry quad, pixel,

@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   int* s_spre = s_slen + SEG_MAX;
   // the segment descriptors are loaded first so their latency overlaps the
   // tile scan
-  const int nseg = __ldcg(A.tile_cursor + t);
+  const int nseg = (int)A.seg_stride;  // one slot per preprocess CTA (length 0: empty)
   const int2* sg = A.seg + (int64_t)t * A.seg_stride;
   const bool seg_fast = nseg <= SEG_MAX;
   int2 dsc[SEG_MAX / RS_T];

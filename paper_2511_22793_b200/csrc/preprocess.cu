@@ -39,8 +39,8 @@ __device__ __forceinline__ double np_floor_div16(double v) { return floor(v / 16
 
 // Tile binning is fused in (the counting-sort digit of rasterizer.py:115-145's
 // per-tile lists): every CTA histograms its Gaussians' tile rectangles,
-// reserves one contiguous stage range for all of them, registers one
-// segment {offset, length} per touched tile and scatters its packed pairs
+// reserves one contiguous stage range for all of them, writes one segment
+// {offset, length} per tile into its own slot and scatters its packed pairs
 // (coarse depth << 32 | index).  Order inside a tile is irrelevant: K3 sorts
 // each tile's gathered segments by the full key.
 __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
@@ -275,15 +275,12 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   __syncthreads();
   const int base = s_base;
   const bool fits = (int64_t)base + total <= A.capacity;
+  // segment slot = this CTA's index (no returning atomics); empty
+  // segments have length 0
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
     const int v = s_tiles[t];
-    if (v) {
-      atomicAdd(A.tile_count + t, v);
-      if (fits) {
-        const int slot = atomicAdd(A.tile_cursor + t, 1);
-        A.seg[(int64_t)t * A.seg_stride + slot] = make_int2(base + s_off[t], v);
-      }
-    }
+    if (v) atomicAdd(A.tile_count + t, v);
+    if (fits) A.seg[(int64_t)t * A.seg_stride + blockIdx.x] = make_int2(base + s_off[t], v);
     s_off[t] += base;
   }
   __syncthreads();
