@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -177,6 +178,10 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   L.off_stage = take(8 * pair_capacity);
   L.off_seg = take(8 * (int64_t)L.ntiles * L.seg_stride);
   L.pxw_chunks = dtype == GSPARC_F32 ? PXW_CHUNKS : 0;
+  if (const char* e = getenv("GSPARC_PXW_CHUNKS")) {  // tests: force the recompute path
+    const int v = atoi(e);
+    if (v >= 0 && v < L.pxw_chunks) L.pxw_chunks = v;
+  }
   L.off_pxw = take(4 * 2 * (int64_t)L.ntiles * L.pxw_chunks * 128 * 32);
   L.off_ch_wm = take(dtype == GSPARC_F32 ? 4 * 4 * L.ch_slots : 0);
   L.total_bytes = o;

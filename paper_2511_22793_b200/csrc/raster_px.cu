@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         }
         const int64_t o = (slot0 + k) * PX_K + e;
         A.ch_idx[o] = idx;
-        A.ch_rec[2 * o] = r0;
-        A.ch_rec[2 * o + 1] = r1p;
+        if (!SC && k >= A.wmax) {  // pass B recomputes these chunks' weights
+          A.ch_rec[2 * o] = r0;
+          A.ch_rec[2 * o + 1] = r1p;
+        }
       }
       fill += ns;
       if (fill >= PX_K) {
@@ -267,8 +269,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         }
         const int64_t o = (slot0 + c) * PX_K + lane;
         A.ch_idx[o] = 0xffffffffu;
-        A.ch_rec[2 * o] = make_float4(0.f, 0.f, 0.f, 0.f);
-        A.ch_rec[2 * o + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+        if (!SC && c >= A.wmax) {
+          A.ch_rec[2 * o] = make_float4(0.f, 0.f, 0.f, 0.f);
+          A.ch_rec[2 * o + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+        }
       }
       publish(c, fill);
       ++c;
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       const int n = *(volatile int*)&s_hdr[s];
       if (n < 0) break;
       const long long tc0 = clock64();
-      A.ch_T[(slot0 + c) * 128 + warp * 32 + lane] = T;  // checkpoint for pass B
+      if (!SC && c >= A.wmax) A.ch_T[(slot0 + c) * 128 + warp * 32 + lane] = T;  // pass B restart
       // the pixel's 32 blending weights of this chunk, stored for pass B
       // (coalesced: entry quad j of the CTA's 128 pixels is one 2 KB row)
       const bool wst = !SC && c < A.wmax;

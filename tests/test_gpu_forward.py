@@ -210,6 +210,29 @@ def test_lazy_tensor_core_path_against_oracle(n, F, R, pose):
     assert d.max() <= 1e-5 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("pxw", ["0", "1"])
+def test_pass_b_recompute_path(pxw, R, pose, monkeypatch):
+    """Pass B normally loads pass A's stored weights; chunks beyond the
+    frame's pxw_chunks recompute them from the T checkpoints.  Force that
+    path (all chunks / all but the first) and compare with the oracle and
+    the stored-weight path."""
+    from paper_2511_22793_b200 import DeviceCloud
+    oc = O.bench_scene(3000, F=8)
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    tx = O.sample_tx(5, 1)
+    ref, aux_ref = O.forward(oc, RX, W, tx[0], 360, 90, threads=8)
+    a, fa = R.rasterize_forward_batch(dc, pose, tx, 360, 90, lazy=True)
+    assert int(fa.layout.pxw_chunks) == 32
+    monkeypatch.setenv("GSPARC_PXW_CHUNKS", pxw)
+    b, fb = R.rasterize_forward_batch(dc, pose, tx, 360, 90, lazy=True)
+    assert int(fb.layout.pxw_chunks) == int(pxw)
+    cnt = fb.contrib_count().cpu().numpy()
+    assert_image_parity(b[0].cpu().numpy(), ref, cnt, aux_ref.contrib_count,
+                        F32_TOL)
+    assert np.array_equal(cnt, fa.contrib_count().cpu().numpy())
+    assert normwise(b[0].cpu().numpy(), a[0].cpu().numpy()) <= 1e-6
+
+
 def test_deterministic_and_dtype(R, pose):
     oc = O.perturbed_scene(64, seed=13)
     a, _ = R.rasterize_forward(host_cloud(oc), pose, [0, 1, 0.5], 180, 45)
