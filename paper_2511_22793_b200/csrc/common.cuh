@@ -210,6 +210,9 @@ struct FastAlpha {
   float alpha, raw, g, dx, dy;
 };
 
+// r1.y = log2(opacity): alpha_raw = 2^(q' + log2 opacity) saves the multiply.
+// fast_alpha_full (backward) evaluates alpha_raw with exactly the forward's
+// operations, and g = 2^q' separately.
 __device__ __forceinline__ FastAlpha fast_alpha_full(float pcx, float pcy, float4 r0, float4 r1,
                                                      float w, float inv_w) {
   FastAlpha o;
@@ -217,9 +220,9 @@ __device__ __forceinline__ FastAlpha fast_alpha_full(float pcx, float pcy, float
   o.dx = fmaf(-w, rintf(dxr * inv_w), dxr);
   o.dy = pcy - r0.y;
   const float t = fmaf(r0.w, o.dy, r0.z * o.dx);
-  const float qp = fmaf(o.dx, t, (r1.x * o.dy) * o.dy);
-  o.g = ex2_approx(qp);
-  o.raw = r1.y * o.g;
+  const float qcy = r1.x * o.dy;
+  o.raw = ex2_approx(fmaf(o.dx, t, fmaf(qcy, o.dy, r1.y)));
+  o.g = ex2_approx(fmaf(o.dx, t, qcy * o.dy));
   const float a = fminf(o.raw, ALPHA_MAX_F);
   o.alpha = a < ALPHA_MIN_F ? 0.f : a;
   return o;
@@ -231,8 +234,7 @@ __device__ __forceinline__ float fast_alpha(float pcx, float pcy, float4 r0, flo
   const float dx = fmaf(-w, rintf(dxr * inv_w), dxr);
   const float dy = pcy - r0.y;
   const float t = fmaf(r0.w, dy, r0.z * dx);
-  const float qp = fmaf(dx, t, (r1.x * dy) * dy);
-  const float a = fminf(r1.y * ex2_approx(qp), ALPHA_MAX_F);
+  const float a = fminf(ex2_approx(fmaf(dx, t, fmaf(r1.x * dy, dy, r1.y))), ALPHA_MAX_F);
   return a < ALPHA_MIN_F ? 0.f : a;
 }
 

@@ -229,7 +229,9 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
       }
       A.rrec[2 * i] = make_float4((float)mx, (float)my, (float)(-0.5 * LOG2E * ca_),
                                   (float)(-LOG2E * cb_));
-      A.rrec[2 * i + 1] = make_float4((float)(-0.5 * LOG2E * cc_), (float)opac, xr, yr);
+      // opacity enters the f32 raster as log2(opacity), folded into the
+      // exponent: alpha_raw = 2^(q' + log2 opacity)
+      A.rrec[2 * i + 1] = make_float4((float)(-0.5 * LOG2E * cc_), (float)log2(opac), xr, yr);
     }
     if (A.rec64) {
       double* r = A.rec64 + 8 * i;

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
         s_fr[2 * tid] = f0;
         s_fr[2 * tid + 1] = f1;
         const float k2 = (float)(-2.0 / LOG2E), k1 = (float)(-1.0 / LOG2E);
-        s_rec[tid] = Rec<R>{f0.x, f0.y, f0.z * k2, f0.w * k1, f1.x * k2, f1.y};
+        s_rec[tid] = Rec<R>{f0.x, f0.y, f0.z * k2, f0.w * k1, f1.x * k2, exp2f(f1.y)};
       } else {
         s_rec[tid] = load_rec_t<R>(A.rec32, A.rec64, idx);
       }

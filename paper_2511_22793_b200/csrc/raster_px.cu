@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         b = __ldg(A.rrec + 2 * (size_t)i + 1);
       } else {
         a = make_float4(0.f, 0.f, 0.f, 0.f);
-        b = make_float4(0.f, 0.f, -1.f, -1.f);
+        b = make_float4(0.f, -INFINITY, -1.f, -1.f);
       }
     };
     uint32_t qi[DI];
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     if (fill > 0) {  // zero-opacity padding: alpha = 0, never included
       if (lane >= fill) {
         s_ring[c % PX_RING][lane][0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_ring[c % PX_RING][lane][1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+        s_ring[c % PX_RING][lane][1] = make_float4(0.f, -INFINITY, __int_as_float(-1), __int_as_float(-1));
         if (SC) {
 #pragma unroll
           for (int ch = 0; ch < SCW; ++ch) s_cf[c % PX_RING][lane][ch] = 0.f;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         A.ch_idx[o] = 0xffffffffu;
         if (!SC && c >= A.wmax) {
           A.ch_rec[2 * o] = make_float4(0.f, 0.f, 0.f, 0.f);
-          A.ch_rec[2 * o + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+          A.ch_rec[2 * o + 1] = make_float4(0.f, -INFINITY, __int_as_float(-1), __int_as_float(-1));
         }
       }
       publish(c, fill);
@@ -591,9 +591,9 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       } else {
         nu = __popc(used);
         lm = nu >= 32 ? 0xffffffffu : (1u << nu) - 1u;
-        if (lane >= nu) {  // padding slots: zero opacity, alpha = 0
+        if (lane >= nu) {  // padding slots: zero opacity (log2 = -inf), alpha = 0
           rs[2 * lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-          rs[2 * lane + 1] = make_float4(0.f, 0.f, __int_as_float(-1), __int_as_float(-1));
+          rs[2 * lane + 1] = make_float4(0.f, -INFINITY, __int_as_float(-1), __int_as_float(-1));
           cidx[lane] = -1;
         }
         if ((used >> lane) & 1u) {  // used entries, in list order
