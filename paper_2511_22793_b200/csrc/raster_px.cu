@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
           } else {
             wq[k] = wgt;
           }
-          Tl = act ? Tl * (1.f - a) : Tl;
+          Tl = act ? fmaf(-Tl, a, Tl) : Tl;  // T (1 - alpha), one rounding
           actm |= act ? (1u << k) : 0u;
         }
         T = Tl;
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
               const float a = fast_alpha(pcx, pcy, rs[2 * e], rs[2 * e + 1], wf, inv_w);
               const bool act = T >= teps && a > 0.f;
               wv[e] = act ? T * a : 0.f;
-              T = act ? T * (1.f - a) : T;
+              T = act ? fmaf(-T, a, T) : T;
             }
           }
         }
