@@ -174,7 +174,7 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   const int64_t det_chunks = channels >= 4 ? (channels + 3) / 4 : 1;
   L.off_det_gcoef = det ? take(esz * pair_capacity * 4 * channels) : 0;
   L.off_det_ggeo = det ? take(esz * pair_capacity * 4 * det_chunks * 6) : 0;
-  L.seg_stride = (nn + PREP_T - 1) / PREP_T;
+  L.seg_stride = (nn + PREP_G - 1) / PREP_G;
   L.off_stage = take(8 * pair_capacity);
   L.off_seg = take(8 * (int64_t)L.ntiles * L.seg_stride);
   L.pxw_chunks = dtype == GSPARC_F32 ? PXW_CHUNKS : 0;

@@ -21,7 +21,8 @@
 namespace gs {
 
 constexpr int TILE = 16;
-constexpr int PREP_T = 128;      // k_preprocess CTA size = Gaussians per staged segment set
+constexpr int PREP_T = 256;      // k_preprocess CTA size (two lanes per Gaussian)
+constexpr int PREP_G = PREP_T / 2;  // Gaussians per k_preprocess CTA (= per staged segment set)
 constexpr int PXW_CHUNKS = 32;  // chunks per pass-A CTA whose weights are stored for pass B
 constexpr int TILE_PX = TILE * TILE;
 constexpr double NEAR_PLANE = 0.05;      // geometry.py:27

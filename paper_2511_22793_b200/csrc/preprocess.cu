@@ -52,38 +52,54 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
   __syncthreads();
 
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // Two warps per 32 Gaussians: the even warp runs the view-dependent
+  // chain (projection, pole clamp, J), the odd warp the covariance chain
+  // (quaternion, scales, V = W Sigma W^T) and the opacity, concurrently; the
+  // odd warp's results reach the even warp through shared memory (exact),
+  // which finishes cov2d, the tile rectangle and the records.  Twice the
+  // warps and half the dependent f64 chain per thread of a
+  // one-thread-per-Gaussian mapping, with no divergence inside a warp.
+  __shared__ double s_cov[PREP_T / 64][10][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool cov_lane = (wid & 1) != 0;
+  const int64_t i = (int64_t)blockIdx.x * PREP_G + (wid >> 1) * 32 + lane;
+  const bool valid = i < A.cloud.n;
+  const double* W = A.pose.W;
   bool kept_out = false;
   uint64_t packed = 0;
   int ry0 = 0, ry1 = -1, ra0 = 0, ra1 = -1, rb0 = 0, rb1 = -1;
-  if (i < A.cloud.n) {
+  double x = 0, y = 0, z = 0, depth = 0, theta = 0, mx = 0, my = 0, rho2_u = 0;
+  double J00 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0;
+  bool keep = false;
+  double V[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double opac = 0;
+  if (valid && !cov_lane) {
     const double* P = A.cloud.positions + 3 * i;
-    const double* W = A.pose.W;
     double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
            p2 = sub(P[2], A.pose.rx[2]);
     // (p - rx) @ W.T  (geometry.py:61-64)
-    double x = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
-    double y = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
-    double z = dot3_seq(p0, p1, p2, W[6], W[7], W[8]);
+    x = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
+    y = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
+    z = dot3_seq(p0, p1, p2, W[6], W[7], W[8]);
     double xx = mul(x, x), yy = mul(y, y), zz = mul(z, z);
     double r2 = add(add(xx, yy), zz);
-    double depth = __dsqrt_rn(r2);  // np.linalg.norm(axis=1)
-    bool keep = (depth >= NEAR_PLANE) && (depth <= FAR_PLANE);
+    depth = __dsqrt_rn(r2);  // np.linalg.norm(axis=1)
+    keep = (depth >= NEAR_PLANE) && (depth <= FAR_PLANE);
     // elevation >= -90 deg is a no-op except for NaN (geometry.py:210-212)
     double sn = y / fmax(depth, 1e-30);
     keep = keep && (sn == sn);
 
     // projection (geometry.py:67-80), r == depth
-    double theta = atan2(x, z);
-    double mx = mul(add(theta / A.gc.pi, 1.0), A.gc.w * 0.5);
+    theta = atan2(x, z);
+    mx = mul(add(theta / A.gc.pi, 1.0), A.gc.w * 0.5);
     double c_sn = fmin(fmax(y / depth, -1.0), 1.0);
     double el = asin(c_sn);
-    double my = mul(mul(2.0, el), A.gc.h / A.gc.pi);
+    my = mul(mul(2.0, el), A.gc.h / A.gc.pi);
 
     // pole clamp (geometry.py:98-113, 131-138): points above 89 deg are
     // evaluated at 89 deg with the same azimuth and radius
     double jx = x, jy = y, jz = z;
-    const double rho2_u = add(xx, zz);
+    rho2_u = add(xx, zz);
     double jr2 = r2, rho2 = rho2_u;
     if (el > A.gc.pole_lim) {
       double tgt_rho = mul(depth, A.gc.cos_lim);
@@ -97,13 +113,15 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     double rho = __dsqrt_rn(rho2);
     const double ca = A.gc.ca, ce = A.gc.ce;
     // J (geometry.py:143-148)
-    double J00 = mul(ca, jz) / rho2;
-    double J02 = mul(-ca, jx) / rho2;
+    J00 = mul(ca, jz) / rho2;
+    J02 = mul(-ca, jx) / rho2;
     double r2rho = mul(jr2, rho);
-    double J10 = mul(mul(-ce, jx), jy) / r2rho;
-    double J11 = mul(ce, rho) / jr2;
-    double J12 = mul(mul(-ce, jy), jz) / r2rho;
+    J10 = mul(mul(-ce, jx), jy) / r2rho;
+    J11 = mul(ce, rho) / jr2;
+    J12 = mul(mul(-ce, jy), jz) / r2rho;
 
+  }
+  if (valid && cov_lane) {
     // Sigma = (R diag s)(R diag s)^T (scene.py:84-88, 117-139)
     const double* q = A.cloud.rotations + 4 * i;
     double qn = __dsqrt_rn(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
       for (int c = 0; c < 3; ++c)
         S[r][c] = add(add(mul(M[r][0], M[c][0]), mul(M[r][1], M[c][1])), mul(M[r][2], M[c][2]));
     // V = W S W^T
-    double WS[3][3], V[3][3];
+    double WS[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -148,6 +166,30 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
       for (int c = 0; c < 3; ++c)
         V[r][c] = add(add(mul(WS[r][0], W[3 * c + 0]), mul(WS[r][1], W[3 * c + 1])),
                       mul(WS[r][2], W[3 * c + 2]));
+    const double logit = A.cloud.raw_opacities[i];
+    if (logit >= 0.0) {
+      opac = 1.0 / (1.0 + exp(-logit));
+    } else {
+      double e = exp(logit);
+      opac = e / (1.0 + e);
+    }
+  }
+  if (cov_lane) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s_cov[wid >> 1][3 * r + c][lane] = V[r][c];
+    s_cov[wid >> 1][9][lane] = opac;
+  }
+  __syncthreads();
+  if (!cov_lane) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) V[r][c] = s_cov[wid >> 1][3 * r + c][lane];
+    opac = s_cov[wid >> 1][9][lane];
+  }
+  if (valid && !cov_lane) {
     // cov2d = J V J^T (rasterizer.py:92-95), J row 0 has J01 = 0
     double JV0[3], JV1[3];
 #pragma unroll
@@ -167,14 +209,6 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     double rxr = mul(FOOTPRINT_SIGMA, __dsqrt_rn(a));
     keep = keep && (add(my, ry) >= 0.0) && (sub(my, ry) <= (double)A.gc.h);
 
-    double logit = A.cloud.raw_opacities[i];
-    double opac;
-    if (logit >= 0.0) {
-      opac = 1.0 / (1.0 + exp(-logit));
-    } else {
-      double e = exp(logit);
-      opac = e / (1.0 + e);
-    }
     double phi = atan2(y, __dsqrt_rn(rho2_u));  // mlp.py:88 (unclamped)
 
     // tile rectangle (rasterizer.py:117-141)
@@ -330,7 +364,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   if (cudaMemsetAsync(frame + L.off_counters, 0, zero_end - L.off_counters, st) != cudaSuccess)
     return check_launch("preprocess memset");
   if (cloud.n > 0) {
-    const int blocks = (int)((cloud.n + PREP_T - 1) / PREP_T);
+    const int blocks = (int)((cloud.n + PREP_G - 1) / PREP_G);
     if (blocks > L.seg_stride) {
       set_error("preprocess: frame planned for fewer Gaussians");
       return GSPARC_ERR_ARG;
