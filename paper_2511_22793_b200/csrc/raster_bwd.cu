@@ -45,8 +45,10 @@ template <typename R, int CB, int NB, bool DET>
 __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int P = blockDim.x;              // pixels of this sub-tile
-  R* s_u = (R*)smraw;                    // [CB][P]
-  R* s_wgt = s_u + CB * P;               // [NB][P]
+  const int UP = P + 1;                  // s_u pitch: the GEMM's lanes read
+                                         // different channels, same pixel
+  R* s_u = (R*)smraw;                    // [CB][P + 1]
+  R* s_wgt = s_u + CB * UP;              // [NB][P]
   R* s_coef = s_wgt + NB * P;            // [NB][CB]
   R* s_red = s_coef + NB * CB;           // [NB][6] (DET: [NB][8 warps][6])
   Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6 * (DET ? 8 : 1));  // [NB]
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       v = dL[((b * A.h + py) * (int64_t)A.w + px) * A.C + ch];
     }
     u[c] = v;
-    s_u[c * P + pix] = v;
+    s_u[c * UP + pix] = v;
   }
   const int p = py * A.w + px;
   R T = inside ? ((const R*)A.T_final)[p] : R(1);
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       const int64_t cc = chunk_base + c;
       if (cc >= A.Cp) continue;
       const R* wr = s_wgt + j * P;
-      const R* ur = s_u + c * P;
+      const R* ur = s_u + c * UP;
       R s = R(0);
 #pragma unroll 8
       for (int q = 0; q < P; ++q) s += wr[q] * ur[q];
@@ -232,9 +234,9 @@ template <typename R, int CB, int NB, bool DET>
 static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   const int P = TILE * A.sr;
   constexpr size_t RED = NB * 6 * (DET ? 8 : 1);
-  const size_t smem_max = sizeof(R) * ((size_t)CB * 256 + (size_t)NB * 256 + NB * CB + RED) +
+  const size_t smem_max = sizeof(R) * ((size_t)CB * 257 + (size_t)NB * 256 + NB * CB + RED) +
                           sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
-  const size_t smem = sizeof(R) * ((size_t)CB * P + (size_t)NB * P + NB * CB + RED) +
+  const size_t smem = sizeof(R) * ((size_t)CB * (P + 1) + (size_t)NB * P + NB * CB + RED) +
                       sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
   auto kern = k_raster_bwd<R, CB, NB, DET>;
   static bool attr_set = false;  // one per instantiation; keeps capture clean
