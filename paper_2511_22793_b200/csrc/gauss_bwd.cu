@@ -42,13 +42,15 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int C = A.cloud.mlp_out, H = A.cloud.mlp_hidden, I = A.cloud.mlp_in, P = A.P;
-  // per-warp scratch: x[8] hid[32] pre[32] gpre[32] gs[C]
-  double* sw = (double*)smraw + (size_t)warp * (8 + 96 + C);
+  // per-warp scratch: x[8] hid[32] pre[32] gpre[32] gs[C] acc[P] (the
+  // weight gradients summed over TX, in f64 shared memory)
+  double* sw = (double*)smraw + (size_t)warp * (8 + 96 + C + P);
   double* s_x = sw;
   double* s_hid = sw + 8;
   double* s_pre = sw + 40;
   double* s_gpre = sw + 72;
   double* s_gs = sw + 104;
+  double* s_acc = s_gs + C;
   if (i >= A.cloud.n) return;
   const int64_t n = A.cloud.n;
   G* g = (G*)A.grad;
@@ -83,6 +85,8 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
   const FR* gcoef = (const FR*)A.gcoef + i * A.Cp;
   const double* pos = A.cloud.positions + 3 * i;
   double g_theta = 0.0, g_phi = 0.0, gpd0 = 0.0, gpd1 = 0.0, gpd2 = 0.0;
+  for (int e = lane; e < P; e += 32) s_acc[e] = 0.0;
+  double acc_gpre = 0.0;  // lane h: sum over TX of dL/d pre_h
 
   for (int b = 0; b < A.B; ++b) {
     const double* txb = A.tx + 3 * b;
@@ -115,16 +119,10 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
       double gh = 0.0;
       for (int c = 0; c < C; ++c) gh += (double)W2[c * H + lane] * s_gs[c];
       s_gpre[lane] = s_pre[lane] > 0.0 ? gh : 0.0;
+      acc_gpre += s_gpre[lane];
     }
     __syncwarp();
     if (lane == 0) {
-      double gx3 = 0.0, gx4 = 0.0;
-      for (int h = 0; h < H; ++h) {
-        gx3 += (double)W1[h * I + 3] * s_gpre[h];
-        gx4 += (double)W1[h * I + 4] * s_gpre[h];
-      }
-      g_theta += gx3;
-      g_phi += gx4;
       if (!(draw < NEAR_PLANE)) {  // rasterizer.py:366-368
         gpd0 += g_d * d0 / d;
         gpd1 += g_d * d1 / d;
@@ -144,10 +142,17 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
       } else {
         v = s_gs[e - H * I - H - C * H];
       }
-      if (b == 0) g_w[e] = (G)v;
-      else g_w[e] = (G)((double)g_w[e] + v);
+      s_acc[e] += v;
     }
     __syncwarp();
+  }
+  for (int e = lane; e < P; e += 32) g_w[e] = (G)s_acc[e];
+  // angle gradients: sum_h W1[h, 3|4] * sum_b gpre_b[h] (mlp.py:58-70)
+  {
+    const double a3 = lane < H ? (double)W1[lane * I + 3] * acc_gpre : 0.0;
+    const double a4 = lane < H ? (double)W1[lane * I + 4] * acc_gpre : 0.0;
+    g_theta = warp_sum(a3);
+    g_phi = warp_sum(a4);
   }
   if (lane != 0) return;
 
@@ -344,7 +349,22 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
   }
   if (cloud.n == 0) return GSPARC_OK;
   const int threads = 128;
-  const size_t smem = sizeof(double) * (threads / 32) * (8 + 96 + (size_t)cloud.mlp_out);
+  const size_t smem = sizeof(double) * (threads / 32) * (8 + 96 + (size_t)cloud.mlp_out + A.P);
+  if (smem > 227 * 1024) {
+    set_error("gaussian backward: %d MLP parameters exceed shared memory", A.P);
+    return GSPARC_ERR_UNSUPPORTED;
+  }
+  static size_t attr[4] = {0, 0, 0, 0};
+  auto opt_in = [&](auto kern, int slot) {
+    if (attr[slot] < smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr[slot] = smem;
+    }
+  };
+  opt_in(k_gauss_bwd<double, double>, 0);
+  opt_in(k_gauss_bwd<double, float>, 1);
+  opt_in(k_gauss_bwd<float, double>, 2);
+  opt_in(k_gauss_bwd<float, float>, 3);
   const unsigned blocks = (unsigned)((cloud.n * 32 + threads - 1) / threads);
   if (L.dtype == GSPARC_F64) {
     if (grad_dtype == GSPARC_F64) k_gauss_bwd<double, double><<<blocks, threads, smem, st>>>(A);
