@@ -28,7 +28,10 @@ struct GBwdArgs {
   void* grad;         // flat, grad dtype
   int64_t Cp;
   int P;
+  int lane_tx;  // (5,16,C<=16) head: lane-per-TX MLP backward
 };
+
+constexpr int LANE_TX_JMAX = 12;  // flat MLP rows up to 384 parameters
 
 template <typename G>
 __device__ __forceinline__ void put(G* base, int64_t k, double v) {
@@ -44,7 +47,8 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
   const int C = A.cloud.mlp_out, H = A.cloud.mlp_hidden, I = A.cloud.mlp_in, P = A.P;
   // per-warp scratch: x[8] hid[32] pre[32] gpre[32] gs[C] acc[P] (the
   // weight gradients summed over TX, in f64 shared memory)
-  double* sw = (double*)smraw + (size_t)warp * (8 + 96 + C + P);
+  double* sw = (double*)smraw +
+               (size_t)warp * (A.lane_tx ? (size_t)32 * (2 * 17 + 6 + C + 1) : (size_t)(8 + 96 + C + P));
   double* s_x = sw;
   double* s_hid = sw + 8;
   double* s_pre = sw + 40;
@@ -85,74 +89,185 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
   const FR* gcoef = (const FR*)A.gcoef + i * A.Cp;
   const double* pos = A.cloud.positions + 3 * i;
   double g_theta = 0.0, g_phi = 0.0, gpd0 = 0.0, gpd1 = 0.0, gpd2 = 0.0;
-  for (int e = lane; e < P; e += 32) s_acc[e] = 0.0;
-  double acc_gpre = 0.0;  // lane h: sum over TX of dL/d pre_h
-
-  for (int b = 0; b < A.B; ++b) {
-    const double* txb = A.tx + 3 * b;
-    if (lane < 5) s_x[lane] = lane < 3 ? (double)(FR)txb[lane] : (lane == 3 ? theta : phi);
-    __syncwarp();
-    if (lane < H) {
-      double pre = 0.0;
-      for (int k = 0; k < I; ++k) pre += (double)W1[lane * I + k] * s_x[k];
-      pre += (double)b1[lane];
-      s_pre[lane] = pre;
-      s_hid[lane] = pre > 0.0 ? pre : 0.0;
-    }
-    __syncwarp();
-    const double d0 = pos[0] - txb[0], d1 = pos[1] - txb[1], d2 = pos[2] - txb[2];
-    const double draw = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-    const double d = draw < NEAR_PLANE ? NEAR_PLANE : draw;
-    // s_c, g_s = dL/dcoef / d,  g_d = -sum_c dL/dcoef_c * s_c / d^2
-    double gd_part = 0.0;
-    for (int c = lane; c < C; c += 32) {
-      double s = 0.0;
-      for (int h = 0; h < H; ++h) s += (double)W2[c * H + h] * s_hid[h];
-      s += (double)b2[c];
-      const double gcv = (double)gcoef[(int64_t)b * C + c];
-      s_gs[c] = gcv / d;
-      gd_part -= gcv * s;
-    }
-    const double g_d = warp_sum(gd_part) / (d * d);
-    __syncwarp();
-    if (lane < H) {
-      double gh = 0.0;
-      for (int c = 0; c < C; ++c) gh += (double)W2[c * H + lane] * s_gs[c];
-      s_gpre[lane] = s_pre[lane] > 0.0 ? gh : 0.0;
-      acc_gpre += s_gpre[lane];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      if (!(draw < NEAR_PLANE)) {  // rasterizer.py:366-368
-        gpd0 += g_d * d0 / d;
-        gpd1 += g_d * d1 / d;
-        gpd2 += g_d * d2 / d;
-      }
-    }
-    // weight gradients: W1 | b1 | W2 | b2 (mlp.py:58-66), summed over TX
-    for (int e = lane; e < P; e += 32) {
-      double v;
-      if (e < H * I) {
-        v = s_gpre[e / I] * s_x[e % I];
-      } else if (e < H * I + H) {
-        v = s_gpre[e - H * I];
-      } else if (e < H * I + H + C * H) {
-        const int f = e - H * I - H;
-        v = s_gs[f / H] * s_hid[f % H];
+  if (A.lane_tx) {
+    // ---- MLP backward, lane = TX (mlp.py:48-70 for the (5,16,C) head).
+    // Each lane runs its transmitter's forward + backward in registers;
+    // the weight gradients sum_b gpre_b (x) x_b, gs_b (x) hid_b are then
+    // 32-term dots over the lanes' rows staged in shared memory, owned by
+    // lane e (mod 32) of the flat parameter row, accumulated in registers.
+    constexpr int H16 = 16, I5 = 5, JMAX = LANE_TX_JMAX;
+    double* t_gp = sw;                      // [32][17] dL/d pre
+    double* t_hid = t_gp + 32 * (H16 + 1);  // [32][17] hidden
+    double* t_x = t_hid + 32 * (H16 + 1);   // [32][6]  inputs
+    double* t_gs = t_x + 32 * (I5 + 1);     // [32][C+1] dL/d s
+    const int CP1 = C + 1;
+    double acc[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) acc[j] = 0.0;
+    double gth = 0.0, gph = 0.0, gq0 = 0.0, gq1 = 0.0, gq2 = 0.0;
+    for (int b0 = 0; b0 < A.B; b0 += 32) {
+      const int b = b0 + lane;
+      const bool vb = b < A.B;
+      double x[I5], hid[H16], gh[H16], pre[H16];
+      x[3] = theta;
+      x[4] = phi;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, draw = 1.0, d = 1.0;
+      if (vb) {
+        const double* txb = A.tx + 3 * b;
+        x[0] = (double)(FR)txb[0];
+        x[1] = (double)(FR)txb[1];
+        x[2] = (double)(FR)txb[2];
+        d0 = pos[0] - txb[0];
+        d1 = pos[1] - txb[1];
+        d2 = pos[2] - txb[2];
+        draw = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        d = draw < NEAR_PLANE ? NEAR_PLANE : draw;
       } else {
-        v = s_gs[e - H * I - H - C * H];
+        x[0] = x[1] = x[2] = 0.0;
       }
-      s_acc[e] += v;
+#pragma unroll
+      for (int h = 0; h < H16; ++h) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < I5; ++k) v += (double)W1[h * I5 + k] * x[k];
+        v += (double)b1[h];
+        pre[h] = v;
+        hid[h] = v > 0.0 ? v : 0.0;
+        gh[h] = 0.0;
+      }
+      double gd_part = 0.0;
+      for (int c = 0; c < C; ++c) {
+        double sc = 0.0;
+#pragma unroll
+        for (int h = 0; h < H16; ++h) sc += (double)W2[c * H16 + h] * hid[h];
+        sc += (double)b2[c];
+        const double gcv = vb ? (double)gcoef[(int64_t)b * C + c] : 0.0;
+        const double gsc = gcv / d;
+        gd_part -= gcv * sc;
+#pragma unroll
+        for (int h = 0; h < H16; ++h) gh[h] += (double)W2[c * H16 + h] * gsc;
+        t_gs[lane * CP1 + c] = gsc;
+      }
+      const double g_d = gd_part / (d * d);
+      if (vb && !(draw < NEAR_PLANE)) {  // rasterizer.py:366-368
+        gq0 += g_d * d0 / d;
+        gq1 += g_d * d1 / d;
+        gq2 += g_d * d2 / d;
+      }
+#pragma unroll
+      for (int h = 0; h < H16; ++h) {
+        const double gp = pre[h] > 0.0 ? gh[h] : 0.0;
+        gth += (double)W1[h * I5 + 3] * gp;
+        gph += (double)W1[h * I5 + 4] * gp;
+        t_gp[lane * (H16 + 1) + h] = gp;
+        t_hid[lane * (H16 + 1) + h] = vb ? hid[h] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < I5; ++k) t_x[lane * (I5 + 1) + k] = x[k];
+      __syncwarp();
+      const int nl = min(32, A.B - b0);
+#pragma unroll
+      for (int j = 0; j < JMAX; ++j) {
+        const int e = lane + 32 * j;
+        if (e >= P) break;
+        double v = 0.0;
+        if (e < H16 * I5) {
+          const int h = e / I5, k = e - h * I5;
+          for (int l = 0; l < nl; ++l) v += t_gp[l * (H16 + 1) + h] * t_x[l * (I5 + 1) + k];
+        } else if (e < H16 * I5 + H16) {
+          const int h = e - H16 * I5;
+          for (int l = 0; l < nl; ++l) v += t_gp[l * (H16 + 1) + h];
+        } else if (e < H16 * I5 + H16 + C * H16) {
+          const int f = e - H16 * I5 - H16, c = f / H16, h = f - c * H16;
+          for (int l = 0; l < nl; ++l) v += t_gs[l * CP1 + c] * t_hid[l * (H16 + 1) + h];
+        } else {
+          const int c = e - H16 * I5 - H16 - C * H16;
+          for (int l = 0; l < nl; ++l) v += t_gs[l * CP1 + c];
+        }
+        acc[j] += v;
+      }
+      __syncwarp();
     }
-    __syncwarp();
-  }
-  for (int e = lane; e < P; e += 32) g_w[e] = (G)s_acc[e];
-  // angle gradients: sum_h W1[h, 3|4] * sum_b gpre_b[h] (mlp.py:58-70)
-  {
-    const double a3 = lane < H ? (double)W1[lane * I + 3] * acc_gpre : 0.0;
-    const double a4 = lane < H ? (double)W1[lane * I + 4] * acc_gpre : 0.0;
-    g_theta = warp_sum(a3);
-    g_phi = warp_sum(a4);
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      const int e = lane + 32 * j;
+      if (e < P) g_w[e] = (G)acc[j];
+    }
+    g_theta = warp_sum(gth);
+    g_phi = warp_sum(gph);
+    gpd0 = warp_sum(gq0);
+    gpd1 = warp_sum(gq1);
+    gpd2 = warp_sum(gq2);
+  } else {
+  for (int e = lane; e < P; e += 32) s_acc[e] = 0.0;
+    double acc_gpre = 0.0;  // lane h: sum over TX of dL/d pre_h
+  
+    for (int b = 0; b < A.B; ++b) {
+      const double* txb = A.tx + 3 * b;
+      if (lane < 5) s_x[lane] = lane < 3 ? (double)(FR)txb[lane] : (lane == 3 ? theta : phi);
+      __syncwarp();
+      if (lane < H) {
+        double pre = 0.0;
+        for (int k = 0; k < I; ++k) pre += (double)W1[lane * I + k] * s_x[k];
+        pre += (double)b1[lane];
+        s_pre[lane] = pre;
+        s_hid[lane] = pre > 0.0 ? pre : 0.0;
+      }
+      __syncwarp();
+      const double d0 = pos[0] - txb[0], d1 = pos[1] - txb[1], d2 = pos[2] - txb[2];
+      const double draw = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+      const double d = draw < NEAR_PLANE ? NEAR_PLANE : draw;
+      // s_c, g_s = dL/dcoef / d,  g_d = -sum_c dL/dcoef_c * s_c / d^2
+      double gd_part = 0.0;
+      for (int c = lane; c < C; c += 32) {
+        double s = 0.0;
+        for (int h = 0; h < H; ++h) s += (double)W2[c * H + h] * s_hid[h];
+        s += (double)b2[c];
+        const double gcv = (double)gcoef[(int64_t)b * C + c];
+        s_gs[c] = gcv / d;
+        gd_part -= gcv * s;
+      }
+      const double g_d = warp_sum(gd_part) / (d * d);
+      __syncwarp();
+      if (lane < H) {
+        double gh = 0.0;
+        for (int c = 0; c < C; ++c) gh += (double)W2[c * H + lane] * s_gs[c];
+        s_gpre[lane] = s_pre[lane] > 0.0 ? gh : 0.0;
+        acc_gpre += s_gpre[lane];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (!(draw < NEAR_PLANE)) {  // rasterizer.py:366-368
+          gpd0 += g_d * d0 / d;
+          gpd1 += g_d * d1 / d;
+          gpd2 += g_d * d2 / d;
+        }
+      }
+      // weight gradients: W1 | b1 | W2 | b2 (mlp.py:58-66), summed over TX
+      for (int e = lane; e < P; e += 32) {
+        double v;
+        if (e < H * I) {
+          v = s_gpre[e / I] * s_x[e % I];
+        } else if (e < H * I + H) {
+          v = s_gpre[e - H * I];
+        } else if (e < H * I + H + C * H) {
+          const int f = e - H * I - H;
+          v = s_gs[f / H] * s_hid[f % H];
+        } else {
+          v = s_gs[e - H * I - H - C * H];
+        }
+        s_acc[e] += v;
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < P; e += 32) g_w[e] = (G)s_acc[e];
+    // angle gradients: sum_h W1[h, 3|4] * sum_b gpre_b[h] (mlp.py:58-70)
+    {
+      const double a3 = lane < H ? (double)W1[lane * I + 3] * acc_gpre : 0.0;
+      const double a4 = lane < H ? (double)W1[lane * I + 4] * acc_gpre : 0.0;
+      g_theta = warp_sum(a3);
+      g_phi = warp_sum(a4);
+    }
   }
   if (lane != 0) return;
 
@@ -349,7 +464,12 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
   }
   if (cloud.n == 0) return GSPARC_OK;
   const int threads = 128;
-  const size_t smem = sizeof(double) * (threads / 32) * (8 + 96 + (size_t)cloud.mlp_out + A.P);
+  A.lane_tx = cloud.mlp_in == 5 && cloud.mlp_hidden == 16 && cloud.mlp_out <= 16 &&
+              A.P <= 32 * LANE_TX_JMAX;
+  const size_t per_warp =
+      A.lane_tx ? (size_t)32 * (2 * 17 + 6 + cloud.mlp_out + 1)
+                : (size_t)(8 + 96 + cloud.mlp_out + A.P);
+  const size_t smem = sizeof(double) * (threads / 32) * per_warp;
   if (smem > 227 * 1024) {
     set_error("gaussian backward: %d MLP parameters exceed shared memory", A.P);
     return GSPARC_ERR_UNSUPPORTED;
