@@ -47,9 +47,10 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   const int P = blockDim.x;              // pixels of this sub-tile
   const int UP = P + 1;                  // s_u pitch: the GEMM's lanes read
                                          // different channels, same pixel
+  const int WP = P + 1;                  // s_wgt pitch (GEMM rows of 4 entries)
   R* s_u = (R*)smraw;                    // [CB][P + 1]
-  R* s_wgt = s_u + CB * UP;              // [NB][P]
-  R* s_coef = s_wgt + NB * P;            // [NB][CB]
+  R* s_wgt = s_u + CB * UP;              // [NB][P + 1]
+  R* s_coef = s_wgt + NB * WP;           // [NB][CB]
   R* s_red = s_coef + NB * CB;           // [NB][6] (DET: [NB][8 warps][6])
   Rec<R>* s_rec = (Rec<R>*)(s_red + NB * 6 * (DET ? 8 : 1));  // [NB]
   int* s_idx = (int*)(s_rec + NB);       // [NB]; bit 31: first copy of a seam duplicate
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
           }
         }
       }
-      s_wgt[j * P + pix] = wgt;
+      s_wgt[j * WP + pix] = wgt;
       const bool any = __any_sync(0xffffffffu, g_sig != R(0) || gc0 != R(0) || gc2 != R(0) ||
                                                    gm0 != R(0) || gm1 != R(0));
       if (any) {
@@ -193,23 +194,51 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       }
     }
     __syncthreads();
-    // dL/dcoef for this batch: [nb x CB] = wgt[nb x 256] . u[256 x CB]
-    for (int o = tid; o < nb * CB; o += blockDim.x) {
-      const int j = o / CB, c = o - j * CB;
-      const int64_t cc = chunk_base + c;
-      if (cc >= A.Cp) continue;
-      const R* wr = s_wgt + j * P;
-      const R* ur = s_u + c * UP;
-      R s = R(0);
-#pragma unroll 8
-      for (int q = 0; q < P; ++q) s += wr[q] * ur[q];
-      const int sj = s_idx[j];
-      if (sj < 0) s = R(0);  // first copy of a seam duplicate
-      if constexpr (DET) {
-        const int64_t k = start + b0 + j;  // list position
-        ((R*)A.dgc)[(k * A.nsub + part) * A.Cp + cc] = s;
-      } else {
-        if (s != R(0)) atomicAdd(gcoef + (int64_t)sj * A.Cp + cc, s);
+    // dL/dcoef for this batch: [nb x CB] = wgt[nb x P] . u[P x CB], register
+    // tiles of 4 entries x CT channels (12 shared loads per 32 FMAs)
+    {
+      constexpr int JT = 4, CT = CB < 8 ? CB : 8;
+      constexpr int NCT = CB / CT, NTILE = (NB / JT) * NCT;
+      for (int tile = tid; tile < NTILE; tile += blockDim.x) {
+        const int j0 = (tile / NCT) * JT, c0 = (tile % NCT) * CT;
+        if (j0 >= nb) continue;
+        R acc[JT][CT];
+#pragma unroll
+        for (int a = 0; a < JT; ++a)
+#pragma unroll
+          for (int b = 0; b < CT; ++b) acc[a][b] = R(0);
+        const R* wr = s_wgt + j0 * WP;
+        const R* ur = s_u + c0 * UP;
+#pragma unroll 4
+        for (int q = 0; q < P; ++q) {
+          R wv[JT], uv[CT];
+#pragma unroll
+          for (int a = 0; a < JT; ++a) wv[a] = wr[a * WP + q];
+#pragma unroll
+          for (int b = 0; b < CT; ++b) uv[b] = ur[b * UP + q];
+#pragma unroll
+          for (int a = 0; a < JT; ++a)
+#pragma unroll
+            for (int b = 0; b < CT; ++b) acc[a][b] += wv[a] * uv[b];
+        }
+#pragma unroll
+        for (int a = 0; a < JT; ++a) {
+          const int j = j0 + a;
+          if (j >= nb) break;
+          const int sj = s_idx[j];
+#pragma unroll
+          for (int b = 0; b < CT; ++b) {
+            const int64_t cc = chunk_base + c0 + b;
+            if (cc >= A.Cp) continue;
+            R v = sj < 0 ? R(0) : acc[a][b];  // first copy of a seam duplicate
+            if constexpr (DET) {
+              const int64_t k = start + b0 + j;  // list position
+              ((R*)A.dgc)[(k * A.nsub + part) * A.Cp + cc] = v;
+            } else {
+              if (v != R(0)) atomicAdd(gcoef + (int64_t)sj * A.Cp + cc, v);
+            }
+          }
+        }
       }
     }
     for (int o = tid; o < nb * 6; o += blockDim.x) {
@@ -234,9 +263,9 @@ template <typename R, int CB, int NB, bool DET>
 static int launch_bwd_cfg(const BwdArgs& A, int ntiles, cudaStream_t st) {
   const int P = TILE * A.sr;
   constexpr size_t RED = NB * 6 * (DET ? 8 : 1);
-  const size_t smem_max = sizeof(R) * ((size_t)CB * 257 + (size_t)NB * 256 + NB * CB + RED) +
+  const size_t smem_max = sizeof(R) * ((size_t)CB * 257 + (size_t)NB * 257 + NB * CB + RED) +
                           sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
-  const size_t smem = sizeof(R) * ((size_t)CB * (P + 1) + (size_t)NB * P + NB * CB + RED) +
+  const size_t smem = sizeof(R) * ((size_t)CB * (P + 1) + (size_t)NB * (P + 1) + NB * CB + RED) +
                       sizeof(Rec<R>) * NB + sizeof(int) * NB + 32 * NB + 32;
   auto kern = k_raster_bwd<R, CB, NB, DET>;
   static bool attr_set = false;  // one per instantiation; keeps capture clean
@@ -377,7 +406,8 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.sr = forward_sub_rows(L, A.Cp);
   A.nsub = TILE / A.sr;
   const size_t esz = L.dtype == GSPARC_F64 ? 8 : 4;
-  const int CB = L.dtype == GSPARC_F64 ? 4 : A.Cp <= 2 ? 2 : A.Cp <= 8 ? 8 : A.Cp <= 16 ? 16 : 32;
+  const int CB = L.dtype == GSPARC_F64 ? 4
+                 : A.Cp <= 2 ? 2 : A.Cp <= 8 ? 8 : A.Cp <= 16 ? 16 : A.Cp <= 32 ? 32 : 64;
   A.nchunks = (int)((A.Cp + CB - 1) / CB);
   if (det) {
     if (A.nsub > 4 || A.nchunks > (L.channels >= 4 ? (L.channels + 3) / 4 : 1)) {
@@ -402,9 +432,12 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   } else if (A.Cp <= 16) {
     rc = det ? launch_bwd_cfg<float, 16, 32, true>(A, L.ntiles, st)
              : launch_bwd_cfg<float, 16, 32, false>(A, L.ntiles, st);
-  } else {
+  } else if (A.Cp <= 32) {
     rc = det ? launch_bwd_cfg<float, 32, 32, true>(A, L.ntiles, st)
              : launch_bwd_cfg<float, 32, 32, false>(A, L.ntiles, st);
+  } else {  // one pass of the alpha/T walk per 64 channels
+    rc = det ? launch_bwd_cfg<float, 64, 32, true>(A, L.ntiles, st)
+             : launch_bwd_cfg<float, 64, 32, false>(A, L.ntiles, st);
   }
   if (rc != GSPARC_OK || !det) return rc;
   RedArgs R;
