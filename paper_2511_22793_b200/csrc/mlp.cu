@@ -127,7 +127,9 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
     bv[u] = (f < nvec && (lane & 3) == 0) ? __ldg(b2 + (f >> 2)) : 0.f;
   }
   const int q = lane & 3;
-  const double* p = A.pos + 3 * i;
+  const double* pp = A.pos + 3 * i;
+  const double pv[3] = {__ldg(pp), __ldg(pp + 1), __ldg(pp + 2)};  // issued with the weights
+  const double* p = pv;
   for (int b = 0; b < A.B; ++b) {
     const double* txb = A.tx + 3 * b;
     float x[5] = {(float)txb[0], (float)txb[1], (float)txb[2], r1.z, r1.w};
@@ -161,9 +163,13 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
   if (A.live_list) {  // one warp per live Gaussian, all in flight
-    for (int64_t gi = wid; gi < count; gi += nwarps) mlp_wide_one(A, A.live_list[gi], lane);
+    // the list entry is read speculatively together with the count (the
+    // list has room for n entries), saving one dependent round trip
+    const int first = wid < A.n ? __ldcg(A.live_list + wid) : 0;
+    const int64_t count = __ldcg(A.counters + GSPARC_CNT_LIVE);
+    for (int64_t gi = wid; gi < count; gi += nwarps)
+      mlp_wide_one(A, gi == wid ? first : __ldcg(A.live_list + gi), lane);
     return;
   }
   for (int64_t gi = wid; gi < A.n; gi += nwarps) {
