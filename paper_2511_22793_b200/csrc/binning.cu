@@ -341,31 +341,47 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   uint64_t* g = A.pairs + s;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
   if (seg_fast && n <= RS_CAP) {
-    // every entry finds its segment by binary search over the length
-    // prefix; all loads of a thread are in flight together
+    // thread t gathers keys [t*per, t*per + per): one binary search over the
+    // segment prefix for its first key, then it walks forward through the
+    // (on average longer than per) segments; all its loads are in flight
+    // together
     block_exclusive_scan(s_slen, s_spre, nseg, sc + A.ntiles + 1);
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 8] = clock64() - t_dbg0;
+    const int per = (n + RS_T - 1) / RS_T;  // <= RS_E
+    const int j0 = threadIdx.x * per;
     uint64_t v[RS_E];
+    if (j0 < n) {
+      int l = 0;  // last segment with prefix <= j0
 #pragma unroll
-    for (int e = 0; e < RS_E; ++e) {
-      const int j = threadIdx.x + e * RS_T;
-      v[e] = 0;
-      if (j < n) {
-        int l = 0;  // last segment with prefix <= j (fixed steps: the
-                    // searches of a thread's keys interleave)
+      for (int step = SEG_MAX / 2; step >= 1; step >>= 1)
+        if (l + step < nseg && s_spre[l + step] <= j0) l += step;
+      int sbeg = s_spre[l], send = sbeg + s_slen[l], soff = s_soff[l];
 #pragma unroll
-        for (int step = SEG_MAX / 2; step >= 1; step >>= 1)
-          if (l + step < nseg && s_spre[l + step] <= j) l += step;
-        v[e] = __ldcg(A.stage + s_soff[l] + (j - s_spre[l]));
+      for (int e = 0; e < RS_E; ++e) {
+        const int j = j0 + e;
+        v[e] = 0;
+        if (e < per && j < n) {
+          while (j >= send) {  // next non-empty segment
+            ++l;
+            sbeg = s_spre[l];
+            send = sbeg + s_slen[l];
+            soff = s_soff[l];
+          }
+          v[e] = __ldcg(A.stage + soff + (j - sbeg));
+        }
       }
     }
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_dbg0;
+    if (j0 < n) {
 #pragma unroll
-    for (int e = 0; e < RS_E; ++e) {
-      const int j = threadIdx.x + e * RS_T;
-      if (j < n) {
-        s_keys[j] = v[e];
-        const uint32_t c = (uint32_t)(v[e] >> 32);
-        lo = min(lo, c);
-        hi = max(hi, c);
+      for (int e = 0; e < RS_E; ++e) {
+        const int j = j0 + e;
+        if (e < per && j < n) {
+          s_keys[j] = v[e];
+          const uint32_t c = (uint32_t)(v[e] >> 32);
+          lo = min(lo, c);
+          hi = max(hi, c);
+        }
       }
     }
   } else {  // one thread per staged segment (any order, the sort is total)

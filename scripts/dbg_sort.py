@@ -17,10 +17,10 @@ L = _lib.lib()
 n = 138
 host = (ctypes.c_longlong * (n * 16))()
 assert L.gsparc_debug_copy(host, ctypes.c_int64(n * 16)) == 0
-d = np.ctypeslib.as_array(host).reshape(n, 16)[:, :8]
+d = np.ctypeslib.as_array(host).reshape(n, 16)[:, :10]
 ts = frame.view("tile_start", torch.int32, (n + 1,)).cpu().numpy()
 ln = np.diff(ts)
-print("phase ends: prologue gather hist scan+scatter insertion warp-buckets ties+write")
+print("phase ends: prologue gather hist scan+scatter rank - ties+write | seg-scan search+load-issue")
 print("avg", d.mean(0).astype(int))
 for r in np.argsort(-d[:, 7])[:6]:
     print("tile", r, "n", ln[r], d[r].astype(int))
