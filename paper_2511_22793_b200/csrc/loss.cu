@@ -33,12 +33,15 @@ struct LossArgsT {
   double* H5;    // [5][NI][S][h][w]
   double* G3;    // [3][NI][S][h][w]
   double* A3;    // [3][NI][S][h][w]
-  double* sums;  // [NI * S][3] per-plane (ssim, l1, sq) sums
+  double* XY;    // [2][NI][S][h][w] prediction and ground truth (f64)
+  double* sums;  // [NI * S][LOSS_RB][3] per-plane partial (ssim, l1, sq) sums
   double* V3;    // [3][tot] per-pixel (ssim, l1, sq) terms
   double* stats; // [NI][4]
   int NI, S, C, h, w, sup;
   double lam;
 };
+
+constexpr int LOSS_RB = 16;  // CTAs per (image, channel) plane in k_loss_reduce
 
 __device__ __forceinline__ int refl(int j, int n) {
   if (j < 0) return -j - 1;
@@ -57,19 +60,31 @@ __device__ __forceinline__ double gt_at(const LossArgsT<T>& A, int b, int s, int
   return (double)A.gt[(((int64_t)b * A.h + r) * A.w + c) * A.S + s];
 }
 
+// prediction (|z| for magnitude supervision) and ground truth once per pixel
+// (the blur reads each 11 times); indices fit 32 bits (checked on launch)
+template <typename T>
+__global__ void k_loss_prep(LossArgsT<T> A) {
+  const int plane = A.h * A.w, tot = A.NI * A.S * plane;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tot) return;
+  const int c = e % A.w, r = (e / A.w) % A.h, bs = e / plane;
+  const int s = bs % A.S, b = bs / A.S;
+  A.XY[e] = pred_at(A, b, s, r, c);
+  A.XY[tot + e] = gt_at(A, b, s, r, c);
+}
+
 template <typename T>
 __global__ void k_loss_h(LossArgsT<T> A) {
-  const int64_t plane = (int64_t)A.h * A.w;
-  const int64_t tot = (int64_t)A.NI * A.S * plane;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int plane = A.h * A.w, tot = A.NI * A.S * plane;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= tot) return;
-  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
-  const int64_t bs = e / plane;
-  const int s = (int)(bs % A.S), b = (int)(bs / A.S);
+  const int c = e % A.w;
+  const int rowbase = e - c;
   double a[5] = {0, 0, 0, 0, 0};
+#pragma unroll
   for (int t = 0; t < 11; ++t) {
     const int cc = refl(c + t - 5, A.w);
-    const double x = pred_at(A, b, s, r, cc), y = gt_at(A, b, s, r, cc);
+    const double x = A.XY[rowbase + cc], y = A.XY[tot + rowbase + cc];
     const double wt = A.win[t];
     a[0] += wt * x;
     a[1] += wt * y;
@@ -77,27 +92,23 @@ __global__ void k_loss_h(LossArgsT<T> A) {
     a[3] += wt * (y * y);
     a[4] += wt * (x * y);
   }
-  for (int k = 0; k < 5; ++k) A.H5[k * tot + e] = a[k];
+  for (int k = 0; k < 5; ++k) A.H5[(int64_t)k * tot + e] = a[k];
 }
 
 template <typename T>
 __global__ void k_loss_v(LossArgsT<T> A) {
-  const int64_t plane = (int64_t)A.h * A.w;
-  const int64_t tot = (int64_t)A.NI * A.S * plane;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int plane = A.h * A.w, tot = A.NI * A.S * plane;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   double ssim_v = 0.0, l1_v = 0.0, sq_v = 0.0;
-  int b = 0, s = 0;
   if (e < tot) {
-    const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
-    const int64_t bs = e / plane;
-    s = (int)(bs % A.S);
-    b = (int)(bs / A.S);
-    const int64_t rowbase = bs * plane;
+    const int c = e % A.w, r = (e / A.w) % A.h;
+    const int bs = e / plane;
+    const int64_t rowbase = (int64_t)bs * plane;
     double m[5] = {0, 0, 0, 0, 0};
     for (int t = 0; t < 11; ++t) {
       const int rr = refl(r + t - 5, A.h);
       const double wt = A.win[t];
-      for (int k = 0; k < 5; ++k) m[k] += wt * A.H5[k * tot + rowbase + (int64_t)rr * A.w + c];
+      for (int k = 0; k < 5; ++k) m[k] += wt * A.H5[(int64_t)k * tot + rowbase + (int64_t)rr * A.w + c];
     }
     const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
     const double mx = m[0], my = m[1];
@@ -108,10 +119,10 @@ __global__ void k_loss_v(LossArgsT<T> A) {
     const double da1 = a2 / (b1 * b2), da2 = a1 / (b1 * b2);
     const double db1 = -sv / b1, db2 = -sv / b2;
     A.G3[e] = 2 * my * da1 - 2 * my * da2 + 2 * mx * db1 - 2 * mx * db2;
-    A.G3[tot + e] = db2;
-    A.G3[2 * tot + e] = 2 * da2;
+    A.G3[(int64_t)tot + e] = db2;
+    A.G3[2 * (int64_t)tot + e] = 2 * da2;
     ssim_v = sv;
-    const double x = pred_at(A, b, s, r, c), y = gt_at(A, b, s, r, c);
+    const double x = A.XY[e], y = A.XY[tot + e];
     l1_v = fabs(x - y);
     sq_v = (x - y) * (x - y);
   }
@@ -119,19 +130,21 @@ __global__ void k_loss_v(LossArgsT<T> A) {
   // k_loss_reduce (no float atomics: the reported losses are bit-stable)
   if (e < tot) {
     A.V3[e] = ssim_v;
-    A.V3[tot + e] = l1_v;
-    A.V3[2 * tot + e] = sq_v;
+    A.V3[(int64_t)tot + e] = l1_v;
+    A.V3[2 * (int64_t)tot + e] = sq_v;
   }
 }
 
-// one CTA per plane: strided per-thread sums, then a fixed shuffle tree
+// LOSS_RB CTAs per plane: fixed strided per-thread sums and a fixed shuffle
+// tree per CTA; k_loss_finalize adds the CTA partials in order
 template <typename T>
 __global__ void __launch_bounds__(256) k_loss_reduce(LossArgsT<T> A) {
   __shared__ double s_part[8][3];
   const int64_t plane = (int64_t)A.h * A.w, tot = (int64_t)A.NI * A.S * plane;
-  const int64_t p = blockIdx.x;
+  const int64_t p = blockIdx.x / LOSS_RB;
+  const int rb = blockIdx.x % LOSS_RB;
   double v[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = threadIdx.x; i < plane; i += blockDim.x) {
+  for (int64_t i = rb * blockDim.x + threadIdx.x; i < plane; i += LOSS_RB * blockDim.x) {
     const int64_t e = p * plane + i;
     v[0] += A.V3[e];
     v[1] += A.V3[tot + e];
@@ -147,7 +160,7 @@ __global__ void __launch_bounds__(256) k_loss_reduce(LossArgsT<T> A) {
   if (threadIdx.x < 3) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_part[w][threadIdx.x];
-    A.sums[p * 3 + threadIdx.x] = t;  // plane p = b * S + s
+    A.sums[(p * LOSS_RB + rb) * 3 + threadIdx.x] = t;  // plane p = b * S + s
   }
 }
 
@@ -172,30 +185,29 @@ __device__ __forceinline__ double adj_line(const LossArgsT<T>& A, const double* 
 
 template <typename T>
 __global__ void k_loss_adj_v(LossArgsT<T> A) {
-  const int64_t plane = (int64_t)A.h * A.w;
-  const int64_t tot = (int64_t)A.NI * A.S * plane;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int plane = A.h * A.w, tot = A.NI * A.S * plane;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= tot) return;
-  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
-  const int64_t bs = e / plane;
+  const int c = e % A.w, r = (e / A.w) % A.h;
+  const int bs = e / plane;
   for (int k = 0; k < 3; ++k)
-    A.A3[k * tot + e] = adj_line(A, A.G3 + k * tot + bs * plane + c, A.w, A.h, r);
+    A.A3[(int64_t)k * tot + e] =
+        adj_line(A, A.G3 + (int64_t)k * tot + (int64_t)bs * plane + c, A.w, A.h, r);
 }
 
 template <typename T>
 __global__ void k_loss_adj_h(LossArgsT<T> A) {
-  const int64_t plane = (int64_t)A.h * A.w;
-  const int64_t tot = (int64_t)A.NI * A.S * plane;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int plane = A.h * A.w, tot = A.NI * A.S * plane;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= tot) return;
-  const int c = (int)(e % A.w), r = (int)((e / A.w) % A.h);
-  const int64_t bs = e / plane;
-  const int s = (int)(bs % A.S), b = (int)(bs / A.S);
-  const double* rowp = A.A3 + bs * plane + (int64_t)r * A.w;
+  const int c = e % A.w, r = (e / A.w) % A.h;
+  const int bs = e / plane;
+  const int s = bs % A.S, b = bs / A.S;
+  const double* rowp = A.A3 + (int64_t)bs * plane + (int64_t)r * A.w;
   const double amx = adj_line(A, rowp, 1, A.w, c);
   const double ab2 = adj_line(A, rowp + tot, 1, A.w, c);
   const double aa2 = adj_line(A, rowp + 2 * tot, 1, A.w, c);
-  const double x = pred_at(A, b, s, r, c), y = gt_at(A, b, s, r, c);
+  const double x = A.XY[e], y = A.XY[tot + e];
   const double n = (double)plane;
   const double gssim = (amx + 2 * x * ab2 + y * aa2) / n;
   const double diff = x - y;
@@ -218,13 +230,16 @@ template <typename T>
 __global__ void k_loss_finalize(LossArgsT<T> A) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= A.NI) return;
-  const double* sm = A.sums + (int64_t)b * A.S * 3;
+  const double* sm = A.sums + (int64_t)b * A.S * LOSS_RB * 3;
   const double n = (double)A.h * A.w;
   double ss = 0.0, l1s = 0.0, sqs = 0.0;
   for (int s = 0; s < A.S; ++s) {
-    ss += sm[3 * s] / n;
-    l1s += sm[3 * s + 1];
-    sqs += sm[3 * s + 2];
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int rb = 0; rb < LOSS_RB; ++rb)
+      for (int k = 0; k < 3; ++k) t[k] += sm[(s * LOSS_RB + rb) * 3 + k];
+    ss += t[0] / n;
+    l1s += t[1];
+    sqs += t[2];
   }
   ss /= A.S;
   const double l1 = l1s / (n * A.S);
@@ -236,7 +251,7 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
 
 int64_t loss_scratch_bytes(int NI, int h, int w, int C) {
   const int64_t tot = (int64_t)NI * C * h * w;  // upper bound: S <= C
-  return (int64_t)sizeof(double) * (14 * tot + (int64_t)NI * C * 3) + 256;
+  return (int64_t)sizeof(double) * (16 * tot + (int64_t)NI * C * 3 * LOSS_RB) + 256;
 }
 
 template <typename T>
@@ -261,11 +276,17 @@ static int run_loss(const T* img, const T* gt, int NI, int h, int w, int C, int 
   A.G3 = A.H5 + 5 * tot;
   A.A3 = A.G3 + 3 * tot;
   A.V3 = A.A3 + 3 * tot;
-  A.sums = A.V3 + 3 * tot;
+  A.XY = A.V3 + 3 * tot;
+  A.sums = A.XY + 2 * tot;
+  if (tot >= (int64_t)1 << 31) {
+    set_error("loss: %lld pixels x channels exceed 2^31", (long long)tot);
+    return GSPARC_ERR_UNSUPPORTED;
+  }
   const unsigned blocks = (unsigned)((tot + 255) / 256);
+  k_loss_prep<T><<<blocks, 256, 0, st>>>(A);
   k_loss_h<T><<<blocks, 256, 0, st>>>(A);
   k_loss_v<T><<<blocks, 256, 0, st>>>(A);
-  k_loss_reduce<T><<<(unsigned)(NI * A.S), 256, 0, st>>>(A);
+  k_loss_reduce<T><<<(unsigned)(NI * A.S * LOSS_RB), 256, 0, st>>>(A);
   k_loss_adj_v<T><<<blocks, 256, 0, st>>>(A);
   k_loss_adj_h<T><<<blocks, 256, 0, st>>>(A);
   k_loss_finalize<T><<<(NI + 127) / 128, 128, 0, st>>>(A);
