@@ -169,8 +169,16 @@ __global__ void __launch_bounds__(256) k_loss_reduce(LossArgsT<T> A) {
 template <typename T>
 __device__ __forceinline__ double adj_line(const LossArgsT<T>& A, const double* g, int stride, int n,
                                           int i) {
+  if (i >= 5 && i + 5 < n) {  // interior: all 11 taps in range, no fold-back
+    const double* gi = g + (int64_t)(i - 5) * stride;
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) acc += A.win[t] * gi[(int64_t)t * stride];
+    return acc;
+  }
   auto G = [&](int j) {
     double acc = 0.0;
+#pragma unroll
     for (int t = 0; t < 11; ++t) {
       const int q = j + t - 5;
       if (q >= 0 && q < n) acc += A.win[t] * g[(int64_t)q * stride];
