@@ -146,8 +146,17 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
           wgt = Tb * a.alpha;
           R uc = R(0);
           const R* cf = s_coef + j * CB;
+          if constexpr (sizeof(R) == 4 && CB % 2 == 0) {  // FFMA2: even/odd partial sums
+            float2 a2 = make_float2(0.f, 0.f);
+            const float2* cf2 = reinterpret_cast<const float2*>(cf);
 #pragma unroll
-          for (int c = 0; c < CB; ++c) uc += u[c] * cf[c];
+            for (int c = 0; c < CB / 2; ++c)
+              a2 = ffma2(make_float2(u[2 * c], u[2 * c + 1]), cf2[c], a2);
+            uc = a2.x + a2.y;
+          } else {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) uc += u[c] * cf[c];
+          }
           const R dA = Tb * uc - suffix / om;
           suffix += wgt * uc;
           T = Tb;
@@ -216,10 +225,22 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
           for (int a = 0; a < JT; ++a) wv[a] = wr[a * WP + q];
 #pragma unroll
           for (int b = 0; b < CT; ++b) uv[b] = ur[b * UP + q];
+          if constexpr (sizeof(R) == 4 && CT % 2 == 0) {  // FFMA2 over channel pairs
 #pragma unroll
-          for (int a = 0; a < JT; ++a)
+            for (int a = 0; a < JT; ++a)
 #pragma unroll
-            for (int b = 0; b < CT; ++b) acc[a][b] += wv[a] * uv[b];
+              for (int b = 0; b < CT; b += 2) {
+                const float2 r2 = ffma2(make_float2(wv[a], wv[a]), make_float2(uv[b], uv[b + 1]),
+                                        make_float2(acc[a][b], acc[a][b + 1]));
+                acc[a][b] = r2.x;
+                acc[a][b + 1] = r2.y;
+              }
+          } else {
+#pragma unroll
+            for (int a = 0; a < JT; ++a)
+#pragma unroll
+              for (int b = 0; b < CT; ++b) acc[a][b] += wv[a] * uv[b];
+          }
         }
 #pragma unroll
         for (int a = 0; a < JT; ++a) {
