@@ -175,29 +175,41 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
       const bool any = __any_sync(0xffffffffu, g_sig != R(0) || gc0 != R(0) || gc2 != R(0) ||
                                                    gm0 != R(0) || gm1 != R(0));
       if (any) {
-        g_sig = warp_sum(g_sig);
-        gc0 = warp_sum(gc0);
-        gc1 = warp_sum(gc1);
-        gc2 = warp_sum(gc2);
-        gm0 = warp_sum(gm0);
-        gm1 = warp_sum(gm1);
-        if (lane == 0) {
+        // reduce-scatter of the 6 values (padded to 8) over the warp: 9
+        // shuffles instead of 6 x 5; lane 4f (f < 6) ends up with field f
+        R v[8] = {gc0, gc1, gc2, gm0, gm1, g_sig, R(0), R(0)};
+        {
+          const bool hi = lane & 16;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // keep 4 (by lane bit 4), send 4
+            const R send = hi ? v[k] : v[k + 4];
+            const R keep = hi ? v[k + 4] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          }
+        }
+        {
+          const bool hi = lane & 8;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {  // keep 2 (by lane bit 3), send 2
+            const R send = hi ? v[k] : v[k + 2];
+            const R keep = hi ? v[k + 2] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+        }
+        {
+          const bool hi = lane & 4;
+          const R send = hi ? v[0] : v[1];
+          const R keep = hi ? v[1] : v[0];
+          v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const int f = lane >> 2;  // (bit4, bit3, bit2) -> field
+        if ((lane & 3) == 0 && f < 6) {
           if constexpr (DET) {  // one slot per warp, summed in warp order
-            R* rr = s_red + (j * 8 + (tid >> 5)) * 6;
-            rr[0] = gc0;
-            rr[1] = gc1;
-            rr[2] = gc2;
-            rr[3] = gm0;
-            rr[4] = gm1;
-            rr[5] = g_sig;
+            s_red[(j * 8 + (tid >> 5)) * 6 + f] = v[0];
           } else {
-            R* rr = s_red + j * 6;
-            atomicAdd(rr + 0, gc0);
-            atomicAdd(rr + 1, gc1);
-            atomicAdd(rr + 2, gc2);
-            atomicAdd(rr + 3, gm0);
-            atomicAdd(rr + 4, gm1);
-            atomicAdd(rr + 5, g_sig);
+            atomicAdd(s_red + j * 6 + f, v[0]);
           }
         }
       }
