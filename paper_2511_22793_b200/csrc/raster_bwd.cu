@@ -142,7 +142,11 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
         }
         if (a.alpha > R(0)) {
           const R om = R(1) - a.alpha;
-          const R Tb = T / om;
+          // one correctly rounded reciprocal for both divisions by (1 - alpha)
+          R rom;
+          if constexpr (sizeof(R) == 4) rom = __frcp_rn(om);
+          else rom = R(1) / om;
+          const R Tb = sizeof(R) == 4 ? T * rom : T / om;
           wgt = Tb * a.alpha;
           R uc = R(0);
           const R* cf = s_coef + j * CB;
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
 #pragma unroll
             for (int c = 0; c < CB; ++c) uc += u[c] * cf[c];
           }
-          const R dA = Tb * uc - suffix / om;
+          const R dA = Tb * uc - (sizeof(R) == 4 ? suffix * rom : suffix / om);
           suffix += wgt * uc;
           T = Tb;
           if (a.raw < amax) {
