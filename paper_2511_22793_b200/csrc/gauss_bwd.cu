@@ -269,9 +269,34 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
       g_phi = warp_sum(a4);
     }
   }
-  if (lane != 0) return;
+  // the per-Gaussian geometry chain runs in k_gauss_geo (thread per
+  // Gaussian); its MLP-side inputs are parked in this Gaussian's own
+  // g_pos / g_ls slots, which that kernel overwrites
+  if (lane == 0) {
+    put(g_pos, 3 * i + 0, gpd0);
+    put(g_pos, 3 * i + 1, gpd1);
+    put(g_pos, 3 * i + 2, gpd2);
+    put(g_ls, 3 * i + 0, g_theta);
+    put(g_ls, 3 * i + 1, g_phi);
+  }
+}
 
-  // ---- geometry chain (f64, lane 0) ----
+// K6b: the per-Gaussian geometry chain (f64), one thread per Gaussian.
+template <typename FR, typename G>
+__global__ void __launch_bounds__(128) k_gauss_geo(GBwdArgs A) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.cloud.n) return;
+  if (A.key[i] == ~0ULL) return;  // culled: zeros written by k_gauss_bwd
+  const int64_t n = A.cloud.n;
+  G* g = (G*)A.grad;
+  G* g_pos = g;
+  G* g_ls = g + 3 * n;
+  G* g_rot = g + 6 * n;
+  G* g_op = g + 10 * n;
+  const double* pos = A.cloud.positions + 3 * i;
+  const double gpd0 = (double)g_pos[3 * i + 0], gpd1 = (double)g_pos[3 * i + 1],
+               gpd2 = (double)g_pos[3 * i + 2];
+  const double g_theta = (double)g_ls[3 * i + 0], g_phi = (double)g_ls[3 * i + 1];
   const double* W = A.pose.W;
   const double p0 = pos[0] - A.pose.rx[0], p1 = pos[1] - A.pose.rx[1], p2 = pos[2] - A.pose.rx[2];
   const double x = p0 * W[0] + p1 * W[1] + p2 * W[2];
@@ -486,12 +511,23 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
   opt_in(k_gauss_bwd<float, double>, 2);
   opt_in(k_gauss_bwd<float, float>, 3);
   const unsigned blocks = (unsigned)((cloud.n * 32 + threads - 1) / threads);
+  const unsigned gblocks = (unsigned)((cloud.n + 127) / 128);
   if (L.dtype == GSPARC_F64) {
-    if (grad_dtype == GSPARC_F64) k_gauss_bwd<double, double><<<blocks, threads, smem, st>>>(A);
-    else k_gauss_bwd<double, float><<<blocks, threads, smem, st>>>(A);
+    if (grad_dtype == GSPARC_F64) {
+      k_gauss_bwd<double, double><<<blocks, threads, smem, st>>>(A);
+      k_gauss_geo<double, double><<<gblocks, 128, 0, st>>>(A);
+    } else {
+      k_gauss_bwd<double, float><<<blocks, threads, smem, st>>>(A);
+      k_gauss_geo<double, float><<<gblocks, 128, 0, st>>>(A);
+    }
   } else {
-    if (grad_dtype == GSPARC_F64) k_gauss_bwd<float, double><<<blocks, threads, smem, st>>>(A);
-    else k_gauss_bwd<float, float><<<blocks, threads, smem, st>>>(A);
+    if (grad_dtype == GSPARC_F64) {
+      k_gauss_bwd<float, double><<<blocks, threads, smem, st>>>(A);
+      k_gauss_geo<float, double><<<gblocks, 128, 0, st>>>(A);
+    } else {
+      k_gauss_bwd<float, float><<<blocks, threads, smem, st>>>(A);
+      k_gauss_geo<float, float><<<gblocks, 128, 0, st>>>(A);
+    }
   }
   return check_launch("k_gauss_bwd");
 }
