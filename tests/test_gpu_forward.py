@@ -176,6 +176,70 @@ def test_against_oracle_at_scale(n, F, kind, R, pose):
                         aux_ref.contrib_count, F32_TOL)
 
 
+def _assert_tiles_match_oracle(aux, aux_ref):
+    got = aux.tile_sources()
+    want = {k: aux_ref.prep.idx[v] for k, v in aux_ref.tiles.items()}
+    assert sorted(got) == sorted(want)
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k
+
+
+def _counter(aux, k):
+    from paper_2511_22793_b200 import _lib
+    return int(aux.frame.counters().cpu()[k])
+
+
+def test_sort_exact_depth_ties(R, pose):
+    """Depth ties broken by source index (np.lexsort((idx, depth))): 150
+    copies of one Gaussian (one K3 bucket of >= 64 keys -> the LSD radix
+    path plus the exact tie fix-up) and sign-mirrored positions with
+    bit-identical radial depth, mixed with a random scene."""
+    base = O.perturbed_scene(400, seed=3)
+    rng = np.random.default_rng(7)
+    n_dup = 150
+    dup = rng.integers(0, base.n)
+    mir = rng.integers(0, base.n, 40)
+    pos = np.concatenate([base.positions, np.repeat(base.positions[dup:dup + 1], n_dup, 0),
+                          base.positions[mir] * np.array([-1.0, 1.0, 1.0]),
+                          base.positions[mir] * np.array([1.0, 1.0, -1.0])])
+    def take(a):
+        return np.concatenate([a, np.repeat(a[dup:dup + 1], n_dup, 0), a[mir], a[mir]])
+    oc = O.Cloud(pos, take(base.log_scales), take(base.rotations),
+                 take(base.raw_opacities), take(base.mlp_weights),
+                 mlp_dims=base.mlp_dims)
+    oc = O.round_f32(oc)
+    tx = O.sample_tx(9, 1)[0]
+    ref, aux_ref = O.forward(oc, RX, W, tx, 180, 45, threads=8)
+    img, aux = R.rasterize_forward(host_cloud(oc), pose, tx, 180, 45)
+    _assert_tiles_match_oracle(aux, aux_ref)
+    assert_image_parity(img.data, ref, aux.contrib_count, aux_ref.contrib_count, F32_TOL)
+
+
+def test_sort_tile_beyond_shared_memory(R, pose):
+    """A tile list longer than K3's shared-memory capacity (8192 keys) takes
+    the in-L2 bitonic path; lists stay bit-exact."""
+    from paper_2511_22793_b200 import _lib
+    rng = np.random.default_rng(11)
+    n = 9000
+    # small Gaussians in front of one tile of a 64x32 image, spread in depth
+    u = rng.uniform(8.0, 16.0, n)
+    v = rng.uniform(2.0, 10.0, n)
+    dirs = np.stack([O.pixel_dir(int(a) % 64, int(b) % 32, 64, 32)
+                     for a, b in zip(u, v)])
+    r = rng.uniform(1.0, 6.0, n)[:, None]
+    base = O.make_uniform([-1, 0, -1], [1, 1, 1], n, seed=5, init_scale=0.02)
+    oc = O.Cloud(dirs * r, base.log_scales, base.rotations, base.raw_opacities - 1.0,
+                 base.mlp_weights * 0.3, mlp_dims=base.mlp_dims)
+    oc = O.round_f32(oc)
+    tx = O.sample_tx(4, 1)[0]
+    ref, aux_ref = O.forward(oc, RX, W, tx, 64, 32, threads=8)
+    assert max(len(v) for v in aux_ref.tiles.values()) > 8192
+    img, aux = R.rasterize_forward(host_cloud(oc), pose, tx, 64, 32)
+    assert _counter(aux, _lib.CNT_BIGTILE) >= 1
+    _assert_tiles_match_oracle(aux, aux_ref)
+    assert_image_parity(img.data, ref, aux.contrib_count, aux_ref.contrib_count, F32_TOL)
+
+
 def test_batched_tx_equals_single(R, pose):
     from paper_2511_22793_b200 import DeviceCloud
     oc = O.bench_scene(2000)
