@@ -115,79 +115,6 @@ __device__ void fix_coarse_ties(uint64_t* a, int n, const uint64_t* key, uint32_
   }
 }
 
-// Register bitonic sort of up to 8192 keys per CTA (1024 threads x 8 keys,
-// blocked layout i = 8*tid + e).  Compare-exchange partners at index
-// distance < 8 are in the same thread, < 256 in the same warp (shuffles),
-// larger go through shared memory.  All comparators put the minimum at the
-// lower index (ascending-only network), so the virtual +inf padding never
-// moves and is never stored.
-constexpr int RB_E = 8;
-constexpr int RB_T = 1024;
-constexpr int RB_CAP = RB_E * RB_T;
-
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
-  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
-  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
-  return ((uint64_t)hi << 32) | lo;
-}
-
-// in-thread compare-exchange of x[e] with x[e ^ D] (D compile time)
-template <int D>
-__device__ __forceinline__ void cx_local(uint64_t (&x)[RB_E]) {
-#pragma unroll
-  for (int e = 0; e < RB_E; ++e) {
-    if ((e ^ D) > e) {
-      const uint64_t a = x[e], b = x[e ^ D];
-      x[e] = a < b ? a : b;
-      x[e ^ D] = a < b ? b : a;
-    }
-  }
-}
-
-// cross-thread step: partner thread t ^ tm; MIRROR pairs element e with the
-// partner's 7 - e (first merge step), otherwise with the partner's e.
-template <bool MIRROR>
-__device__ __forceinline__ void cx_remote(uint64_t (&x)[RB_E], uint64_t* sm, int tm,
-                                          bool lo_half) {
-  const int t = threadIdx.x;
-  uint64_t y[RB_E];
-  if (tm < 32) {
-#pragma unroll
-    for (int e = 0; e < RB_E; ++e) y[e] = shfl64(x[MIRROR ? RB_E - 1 - e : e], (t & 31) ^ tm);
-  } else {
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < RB_E; ++e) sm[t * RB_E + e] = x[e];
-    __syncthreads();
-    const int pt = t ^ tm;
-#pragma unroll
-    for (int e = 0; e < RB_E; ++e) y[e] = sm[pt * RB_E + (MIRROR ? RB_E - 1 - e : e)];
-  }
-#pragma unroll
-  for (int e = 0; e < RB_E; ++e) {
-    const uint64_t a = x[e], b = y[e];
-    x[e] = lo_half ? (a < b ? a : b) : (a < b ? b : a);
-  }
-}
-
-__device__ void reg_bitonic(uint64_t (&x)[RB_E], uint64_t* sm, int np2) {
-  const int t = threadIdx.x;
-  // k = 2, 4, 8: entirely inside the thread (mirror + cleaners)
-  cx_local<1>(x);
-  cx_local<3>(x);
-  cx_local<1>(x);
-  cx_local<7>(x);
-  cx_local<2>(x);
-  cx_local<1>(x);
-  for (int k = 16; k <= np2; k <<= 1) {
-    cx_remote<true>(x, sm, (k - 1) >> 3, (t & (k >> 4)) == 0);
-    for (int s = k >> 2; s >= RB_E; s >>= 1) cx_remote<false>(x, sm, s >> 3, (t & (s >> 3)) == 0);
-    cx_local<4>(x);
-    cx_local<2>(x);
-    cx_local<1>(x);
-  }
-}
-
 // Block LSD radix sort of one tile's packed keys (coarse_depth32 << 32 |
 // index) in shared memory on the tile-relative key
 //     d = (coarse - cmin) >> shift   (at most 24 significant bits)

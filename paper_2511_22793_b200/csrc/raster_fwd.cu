@@ -36,7 +36,6 @@ struct RasterArgs {
   const uint64_t* pairs;
   const int* tile_start;
   int* wstop;              // [ntiles * 8] visited prefix per 2-row strip
-  const float4* pair_rec;  // f32 record per list entry (list order)
   const float4* rec32;
   const double* rec64;
   const void* coef;
@@ -125,16 +124,9 @@ __global__ void __launch_bounds__(256) k_raster(RasterArgs A) {
     __syncthreads();
     for (int e = tid; e < CH; e += blockDim.x) {
       if (e < nch) {
-        if constexpr (sizeof(R) == 4) {
-          const float4 a = __ldg(A.pair_rec + 2 * (size_t)(cb + e));
-          const float4 b = __ldg(A.pair_rec + 2 * (size_t)(cb + e) + 1);
-          s_rec[e] = {a.x, a.y, a.z, a.w, b.x, b.y};
-          s_idx[e] = __float_as_int(b.z);
-        } else {
-          const uint32_t idx = (uint32_t)A.pairs[cb + e];
-          s_rec[e] = load_rec_t<R>(A.rec32, A.rec64, idx);
-          s_idx[e] = (int)idx;
-        }
+        const uint32_t idx = (uint32_t)A.pairs[cb + e];
+        s_rec[e] = load_rec_t<R>(A.rec32, A.rec64, idx);
+        s_idx[e] = (int)idx;
       }
       if (AUX) s_live[e] = 0;
     }
@@ -321,7 +313,6 @@ int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, i
   A.pairs = (const uint64_t*)(frame + L.off_pairs);
   A.tile_start = (const int*)(frame + L.off_tile_start);
   A.wstop = (int*)(frame + L.off_wstop);
-  A.pair_rec = (const float4*)(frame + L.off_pair_rec);
   A.rec32 = (const float4*)(frame + L.off_rec32);
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.coef = frame + L.off_coef;
