@@ -119,13 +119,36 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
         s_rec[tid] = load_rec_t<R>(A.rec32, A.rec64, idx);
       }
     }
-    for (int e = tid; e < nb * CB; e += blockDim.x) {
-      const int j = e / CB, c = e - j * CB;
-      const uint32_t idx = (uint32_t)A.pairs[start + b0 + j];
-      const int64_t cc = chunk_base + c;
-      s_coef[e] = cc < A.Cp ? coef[(int64_t)idx * A.Cp + cc] : R(0);
-    }
     for (int e = tid; e < nb * 6 * (DET ? 8 : 1); e += blockDim.x) s_red[e] = R(0);
+    __syncthreads();
+    // the batch's coef rows: indices from shared memory, every load of a
+    // thread issued before its stores (one latency instead of one per row)
+    {
+      constexpr int PER = (NB * CB + 63) / 64;  // elements per thread at P >= 64
+      R cv[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * blockDim.x;
+        cv[k] = R(0);
+        if (e < nb * CB) {
+          const int j = e / CB, c = e - j * CB;
+          const int64_t cc = chunk_base + c;
+          const uint32_t idx = (uint32_t)(s_idx[j] & 0x7fffffff);
+          if (cc < A.Cp) cv[k] = coef[(int64_t)idx * A.Cp + cc];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * blockDim.x;
+        if (e < nb * CB) s_coef[e] = cv[k];
+      }
+      for (int e = tid + PER * blockDim.x; e < nb * CB; e += blockDim.x) {  // P < 64
+        const int j = e / CB, c = e - j * CB;
+        const int64_t cc = chunk_base + c;
+        const uint32_t idx = (uint32_t)(s_idx[j] & 0x7fffffff);
+        s_coef[e] = cc < A.Cp ? coef[(int64_t)idx * A.Cp + cc] : R(0);
+      }
+    }
     __syncthreads();
     for (int j = nb - 1; j >= 0; --j) {
       const int k = b0 + j;
