@@ -173,7 +173,17 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
           wgt = Tb * a.alpha;
           R uc = R(0);
           const R* cf = s_coef + j * CB;
-          if constexpr (sizeof(R) == 4 && CB % 2 == 0) {  // FFMA2: even/odd partial sums
+          if constexpr (sizeof(R) == 4 && CB % 8 == 0) {
+            // FFMA2 with 4 independent accumulators (8 partial sums): a
+            // 4x shorter dependent chain than one running sum
+            float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
+            const float2* cf2 = reinterpret_cast<const float2*>(cf);
+#pragma unroll
+            for (int c = 0; c < CB / 2; ++c)
+              a2[c & 3] = ffma2(make_float2(u[2 * c], u[2 * c + 1]), cf2[c], a2[c & 3]);
+            uc = ((a2[0].x + a2[0].y) + (a2[1].x + a2[1].y)) + ((a2[2].x + a2[2].y) + (a2[3].x + a2[3].y));
+          } else if constexpr (sizeof(R) == 4 && CB % 2 == 0) {  // FFMA2: even/odd partial sums
             float2 a2 = make_float2(0.f, 0.f);
             const float2* cf2 = reinterpret_cast<const float2*>(cf);
 #pragma unroll
