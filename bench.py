@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="c2: fixed-order (bit-reproducible) backward")
     return ap.parse_args()
 
 
@@ -284,6 +286,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     R.check_frame(frame)
+    per_step_launches = count_our_kernels(step_eager) or kernels_per_step(lazy)
     times = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
     total_ms = float(times.sum())
     if dist:
@@ -368,7 +371,7 @@ def run_ours(args):
                     "path": "rasterize_forward_batch(pinned host TX -> device) "
                             "+ D2H of every image into pinned memory on a copy "
                             "stream overlapping the next render"},
-            "gpu_launches": int(args.steps * kernels_per_step(lazy)),
+            "gpu_launches": int(args.steps * per_step_launches),
             "roofline": roof,
             "pipeline_hbm": {"algorithmic_bytes": bytes_fwd,
                              "achieved_gbs": bytes_fwd / (ms / 1e3) / 1e9,
@@ -397,8 +400,25 @@ def run_ours(args):
 
 
 def kernels_per_step(lazy):
-    # preprocess, bin, tile_sort, raster pass(es), mlp (+ memsets are copies)
-    return 6 if lazy else 5
+    # static fallback: preprocess, tile_sort, raster pass(es), mlp
+    return 5 if lazy else 4
+
+
+def count_our_kernels(fn):
+    """Kernels of libgsparc_b200 (names gs::k_*) launched by one call of fn,
+    counted with the CUDA profiler (CUPTI); None if it is unavailable."""
+    import torch
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        n = sum(1 for e in prof.events()
+                if e.device_type.name == "CUDA" and "gs::k_" in e.name)
+        return n if n > 0 else None
+    except Exception:
+        return None
 
 
 def stage_times(R, dc, pose, tx, w, h, frame, img, lazy, flush, reps=20):
@@ -504,7 +524,7 @@ def run_train(args):
     S = 5000                                  # config-4 sized sample table
     txs = sample_tx(7, S)
     gt = np.random.default_rng(7).random((S, h, w, 1), dtype=np.float32) * 0.5
-    cfg = TrainConfig(width=w, height=h, batch_tx=B)
+    cfg = TrainConfig(width=w, height=h, batch_tx=B, deterministic=args.deterministic)
     tr = Trainer(cloud, ViewPose(np.zeros(3)), cfg, txs, gt)
     if not args.no_graph:
         tr.capture()
@@ -533,6 +553,7 @@ def run_train(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
+    per_step = count_our_kernels(lambda: tr.step(batches[0]))
     line = None
     if rank == 0:
         line = {"metric": "train iterations/s (global batch 32 TX)",
@@ -542,10 +563,11 @@ def run_train(args):
                 "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (bench scene, random magnitude targets)",
                 "config": dict(workload_config(args.config),
-                               parallelism=f"dp{world}"),
+                               parallelism=f"dp{world}",
+                               deterministic_backward=bool(args.deterministic)),
                 "clocks": clocks.summary(), "renders_per_s": B * 1e3 / ms,
                 "last_loss": loss, "healthy": bool(ok),
-                "gpu_launches": None}
+                "gpu_launches": int(per_step * args.steps) if per_step else None}
     if dist:
         dist.barrier()
         dist.destroy_process_group()
