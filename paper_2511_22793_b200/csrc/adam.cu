@@ -61,12 +61,19 @@ __device__ double position_lr_dev(double step, const gsparc_adam_config& c) {
 __global__ void k_adam(AdamArgs A, int64_t total) {
   // a frame whose pair buffer overflowed produced no valid gradient
   if (A.counters[GSPARC_CNT_NONFINITE] || A.counters[GSPARC_CNT_OVERFLOW]) return;
-  const int64_t step = *A.step;
-  const double t = (double)(step + 1);
+  // step scalars (pow, exp/log/sin of the position schedule) once per CTA
+  __shared__ double s_sc[3];
+  if (threadIdx.x == 0) {
+    const int64_t step = *A.step;
+    const double t = (double)(step + 1);
+    s_sc[0] = 1.0 - pow(A.cfg.beta1, t);
+    s_sc[1] = 1.0 - pow(A.cfg.beta2, t);
+    s_sc[2] = position_lr_dev((double)step, A.cfg);
+  }
+  __syncthreads();
   const double b1 = A.cfg.beta1, b2 = A.cfg.beta2, eps = A.cfg.eps;
-  const double bc1 = 1.0 - pow(b1, t), bc2 = 1.0 - pow(b2, t);
-  const double lr_pos = position_lr_dev((double)step, A.cfg);
-  const double lrs[5] = {lr_pos, A.cfg.scaling_lr, A.cfg.rotation_lr, A.cfg.opacity_lr,
+  const double bc1 = s_sc[0], bc2 = s_sc[1];
+  const double lrs[5] = {s_sc[2], A.cfg.scaling_lr, A.cfg.rotation_lr, A.cfg.opacity_lr,
                          A.cfg.mlp_lr};
   const int64_t n = A.n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
