@@ -157,6 +157,9 @@ typedef struct gsparc_frame_layout {
   int64_t pxw_chunks;     /* chunks per CTA with stored weights          */
   int64_t off_ch_wm;      /* u32  [slots,4] per 32-pixel warp: entries of
                              the chunk with an included contribution     */
+  int64_t off_det_inv;    /* i32  [n,320] list position of every (Gaussian,
+                             tile of its rectangle) in canonical tile order
+                             (with_backward == 2; written by K3)          */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

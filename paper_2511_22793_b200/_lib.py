@@ -53,7 +53,8 @@ class CLayout(ctypes.Structure):
                 [("ch_slots", c_i64), ("off_ch_used", c_i64),
                  ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64),
                  ("off_stage", c_i64), ("off_seg", c_i64), ("seg_stride", c_i64),
-                 ("off_pxw", c_i64), ("pxw_chunks", c_i64), ("off_ch_wm", c_i64)])
+                 ("off_pxw", c_i64), ("pxw_chunks", c_i64), ("off_ch_wm", c_i64),
+                 ("off_det_inv", c_i64)])
 
 
 class CEmitter(ctypes.Structure):

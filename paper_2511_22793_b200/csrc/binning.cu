@@ -33,6 +33,9 @@ struct SortArgs {
   const int2* seg;
   const uint64_t* stage;
   int64_t seg_stride;
+  int* inv;          // deterministic frames: [n][DET_MAXT] list positions
+  const int4* rect;  // tile rectangles (K2)
+  int ntx;
   int ntiles;
   long long* dbg;  // experiments: per-CTA phase clocks (GSPARC_SORT_DBG)
 };
@@ -438,6 +441,20 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     fix_coarse_ties(g, n, A.key);
     __syncthreads();
   }
+  if (A.inv) {  // deterministic backward: list position of (Gaussian, tile slot)
+    __syncthreads();
+    const int ty = t / A.ntx, tx = t - ty * A.ntx;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint64_t v = g[j];
+      if (j > 0 && g[j - 1] == v) continue;  // second copy of a seam duplicate
+      const uint32_t idx = (uint32_t)v;
+      const int4 rc = __ldg(A.rect + idx);
+      const int y0 = rc.x & 0xffff, a0 = rc.y & 0xffff, a1 = rc.y >> 16, b1 = rc.z >> 16;
+      const int na = a1 - a0 + 1, nbo = b1 >= 0 ? min(b1, a0 - 1) + 1 : 0;
+      const int slot = (ty - y0) * (na + nbo) + (tx >= a0 && tx <= a1 ? tx - a0 : na + tx);
+      if (slot >= 0 && slot < DET_MAXT) A.inv[(int64_t)idx * DET_MAXT + slot] = s + j;
+    }
+  }
 }
 
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
@@ -451,6 +468,9 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.seg = (const int2*)(frame + L.off_seg);
   A.stage = (const uint64_t*)(frame + L.off_stage);
   A.seg_stride = L.seg_stride;
+  A.inv = L.with_backward == 2 ? (int*)(frame + L.off_det_inv) : nullptr;
+  A.rect = (const int4*)(frame + L.off_rect);
+  A.ntx = L.ntx;
   A.ntiles = L.ntiles;
   A.dbg = nullptr;
   if (getenv("GSPARC_SORT_DBG")) {  // experiments only

@@ -24,6 +24,7 @@ constexpr int TILE = 16;
 constexpr int PREP_T = 256;      // k_preprocess CTA size (two lanes per Gaussian)
 constexpr int PREP_G = PREP_T / 2;  // Gaussians per k_preprocess CTA (= per staged segment set)
 constexpr int PXW_CHUNKS = 32;  // chunks per pass-A CTA whose weights are stored for pass B
+constexpr int DET_MAXT = 320;   // deterministic backward: tiles per Gaussian (slots)
 constexpr int TILE_PX = TILE * TILE;
 constexpr double NEAR_PLANE = 0.05;      // geometry.py:27
 constexpr double FAR_PLANE = 1000.0;     // geometry.py:28

@@ -366,9 +366,10 @@ struct RedArgs {
   void* ggeo;
   int64_t n, Cp;
   int nchunks, ntx, nsub;
+  const int* inv;  // [n][DET_MAXT] list positions per tile slot (K3)
 };
 
-constexpr int RED_MAXT = 320;  // tiles per Gaussian (2 x 138 at 90x360 + seam)
+constexpr int RED_MAXT = DET_MAXT;  // tiles per Gaussian (2 x 138 at 90x360 + seam)
 
 template <typename R>
 __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
@@ -398,14 +399,9 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     const int ty = y0 + j / (na + nbo), rj = j % (na + nbo);
     const int tx = rj < na ? a0 + rj : rj - na;
     const int t = ty * A.ntx + tx;
-    int lo = A.tile_start[t], hi = A.tile_start[t + 1];
-    while (lo < hi) {  // first entry not below (ki, i)
-      const int mid = (lo + hi) >> 1;
-      const uint32_t pi = (uint32_t)A.pairs[mid];
-      const uint64_t pk = A.key[pi];
-      if (pk < ki || (pk == ki && pi < (uint32_t)i)) lo = mid + 1;
-      else hi = mid;
-    }
+    // list position of (Gaussian i, tile t): recorded by K3 when it placed
+    // the entry (the first copy of a seam duplicate)
+    const int lo = __ldg(A.inv + i * DET_MAXT + j);
     const bool twice = rj < na && b1 >= 0 && tx <= b1;  // seam duplicate
     s_pos[warp][j] = lo | (twice ? (1 << 30) : 0);
     s_tile[warp][j] = (short)t;
@@ -525,6 +521,7 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   R.nchunks = A.nchunks;
   R.ntx = L.ntx;
   R.nsub = A.nsub;
+  R.inv = (const int*)(frame + L.off_det_inv);
   const unsigned blocks = (unsigned)((L.n + 7) / 8);
   if (blocks == 0) return GSPARC_OK;
   if (L.dtype == GSPARC_F64) k_bwd_reduce<double><<<blocks, 256, 0, st>>>(R);
