@@ -375,6 +375,7 @@ template <typename R>
 __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
   __shared__ int s_pos[8][RED_MAXT];   // list position per enumerated tile
   __shared__ short s_tile[8][RED_MAXT];
+  __shared__ unsigned char s_vis[8][RED_MAXT];  // bit 4 copy + sub-tile: partial visited
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * 8 + warp;
   if (i >= A.n) return;
@@ -403,14 +404,22 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     // the entry (the first copy of a seam duplicate)
     const int lo = __ldg(A.inv + i * DET_MAXT + j);
     const bool twice = rj < na && b1 >= 0 && tx <= b1;  // seam duplicate
-    s_pos[warp][j] = lo | (twice ? (1 << 30) : 0);
+    s_pos[warp][j] = lo;
     s_tile[warp][j] = (short)t;
+    // which (copy, sub-tile) partials exist: K5 wrote those inside each
+    // sub-tile's visited prefix (wstop, per 32-pixel warp)
+    const int ts = A.tile_start[t];
+    unsigned vis = 0;
+    for (int copy = 0; copy <= (twice ? 1 : 0); ++copy)
+      for (int p = 0; p < A.nsub; ++p) {
+        const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
+        if (lo + copy - ts < nv) vis |= 1u << (4 * copy + p);
+      }
+    s_vis[warp][j] = (unsigned char)vis;
   }
   __syncwarp();
-  auto visible = [&](int t, int k, int p) {
-    const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
-    return k - A.tile_start[t] < nv;
-  };
+  // sums in the fixed order (tile slot, copy, sub-tile[, chunk]); the (up to
+  // 8) partials of a slot are loaded together
   const R* dgc = (const R*)A.dgc;
   const R* dgg = (const R*)A.dgg;
   for (int64_t c0 = 0; c0 < A.Cp; c0 += 32) {
@@ -418,12 +427,17 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     R acc = R(0);
     if (cc < A.Cp) {
       for (int j = 0; j < ntile; ++j) {
-        const int pv = s_pos[warp][j], t = s_tile[warp][j];
-        for (int copy = 0; copy <= (pv >> 30); ++copy) {
-          const int k = (pv & ((1 << 30) - 1)) + copy;
-          for (int p = 0; p < A.nsub; ++p)
-            if (visible(t, k, p)) acc += dgc[((int64_t)k * A.nsub + p) * A.Cp + cc];
-        }
+        const int64_t k0 = s_pos[warp][j];
+        const unsigned vis = s_vis[warp][j];
+        R v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          v[q] = ((vis >> q) & 1u)
+                     ? dgc[((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.Cp + cc]
+                     : R(0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if ((vis >> q) & 1u) acc += v[q];
       }
       gc[cc] = acc;
     }
@@ -432,14 +446,12 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     R acc = R(0);
     if (lane < 6) {
       for (int j = 0; j < ntile; ++j) {
-        const int pv = s_pos[warp][j], t = s_tile[warp][j];
-        for (int copy = 0; copy <= (pv >> 30); ++copy) {
-          const int k = (pv & ((1 << 30) - 1)) + copy;
-          for (int p = 0; p < A.nsub; ++p)
-            if (visible(t, k, p))
-              for (int ch = 0; ch < A.nchunks; ++ch)
-                acc += dgg[(((int64_t)k * A.nsub + p) * A.nchunks + ch) * 6 + lane];
-        }
+        const int64_t k0 = s_pos[warp][j];
+        const unsigned vis = s_vis[warp][j];
+        for (int q = 0; q < 8; ++q)
+          if ((vis >> q) & 1u)
+            for (int ch = 0; ch < A.nchunks; ++ch)
+              acc += dgg[(((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.nchunks + ch) * 6 + lane];
       }
     }
     gg[lane] = acc;
