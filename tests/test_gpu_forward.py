@@ -240,6 +240,24 @@ def test_sort_tile_beyond_shared_memory(R, pose):
     assert_image_parity(img.data, ref, aux.contrib_count, aux_ref.contrib_count, F32_TOL)
 
 
+@pytest.mark.parametrize("n,F,w,h", [(2000, 160, 360, 90), (3000, 4, 720, 180)])
+def test_wide_channels_and_large_image(n, F, w, h, R, pose):
+    """320 channels (two 256-wide accumulation CTAs per half-tile, TMEM
+    512 columns, lazy tensor-core path) and a 180x720 hemisphere (540 tiles,
+    raster grids beyond one wave), against the oracle."""
+    from paper_2511_22793_b200 import DeviceCloud
+    oc = O.bench_scene(n, F=F)
+    tx = O.sample_tx(5, 1)
+    ref, aux_ref = O.forward(oc, RX, W, tx[0], w, h, threads=8)
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    b, fb = R.rasterize_forward_batch(dc, pose, tx, w, h, lazy=True)
+    assert_image_parity(b[0].cpu().numpy(), ref, fb.contrib_count().cpu().numpy(),
+                        aux_ref.contrib_count, F32_TOL)
+    img, aux = R.rasterize_forward(host_cloud(oc), pose, tx[0], w, h)
+    _assert_tiles_match_oracle(aux, aux_ref)
+    assert_image_parity(img.data, ref, aux.contrib_count, aux_ref.contrib_count, F32_TOL)
+
+
 def test_batched_tx_equals_single(R, pose):
     from paper_2511_22793_b200 import DeviceCloud
     oc = O.bench_scene(2000)
