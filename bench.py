@@ -39,7 +39,32 @@ CONFIGS = {
     "c3": (50_000, 360, 90, 52, 1),
     "c1": (4_096, 360, 90, 1, 64),
     "c2": (16_384, 360, 90, 1, 32),   # training step (fwd+loss+bwd+Adam)
+    # stress: 500k Gaussians, 180x720 x 256 subcarriers; 4096 TX over 8 GPUs
+    # = 512 per GPU, rendered here 4 per step (geometry shared in a step)
+    "c5": (500_000, 720, 180, 256, 4),
 }
+
+
+def device_bench_cloud(n, F, seed=0):
+    """The bench-scene recipe (cli.py:239-246: uniform positions in
+    [-5,-0.2,-5]x[5,3.2,5], log-scale ln(0.02 |diag|), identity rotations,
+    logit -2, N(0,1) MLP weights x 0.3) drawn on the device with torch's
+    generator -- the 17.6 GB of c5 weights never touch the host."""
+    import torch
+    from paper_2511_22793_b200 import DeviceCloud
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    lo = torch.tensor([-5.0, -0.2, -5.0], dtype=torch.float64, device="cuda")
+    hi = torch.tensor([5.0, 3.2, 5.0], dtype=torch.float64, device="cuda")
+    pos = lo + (hi - lo) * torch.rand((n, 3), generator=g, dtype=torch.float64, device="cuda")
+    diag = float(torch.linalg.norm(hi - lo))
+    ls = torch.full((n, 3), float(np.log(0.02 * diag)), dtype=torch.float64, device="cuda")
+    rot = torch.zeros((n, 4), dtype=torch.float64, device="cuda")
+    rot[:, 0] = 1.0
+    op = torch.full((n, 1), -2.0, dtype=torch.float64, device="cuda")
+    dims = (5, 16, 2 * F)
+    P = 5 * 16 + 16 + 16 * 2 * F + 2 * F
+    mw = torch.randn((n, P), generator=g, dtype=torch.float32, device="cuda") * 0.3
+    return DeviceCloud(pos.contiguous(), ls, rot, op, mw, dims)
 
 
 def parse():
@@ -207,12 +232,16 @@ def workload_config(name):
     desc = {"c3": "config 3: CSI multi-frequency per-TX render latency",
             "c1": "config 1: batched forward of 64 TX positions",
             "c2": "config 2: training step (render + L1/SSIM + backward + "
-                  "Adam) on a batch of 32 TX"}[name]
+                  "Adam) on a batch of 32 TX",
+            "c5": "config 5 (stress): batched render, 4096 TX sharded over "
+                  "the GPUs, 4 TX per step per GPU"}[name]
     return {"workload": f"{desc}; {n} Gaussians, {h}x{w} hemisphere x {F} "
                         f"subcarrier(s) ({2 * F} channels), {B} TX per step",
             "n_gaussians": n, "height": h, "width": w, "subcarriers": F,
             "channels": 2 * F, "tx_per_step": B,
-            "scene": "reference bench scene (cli.py:239-246), GSPC-rounded",
+            "scene": ("bench scene recipe (cli.py:239-246) drawn on the device"
+                      if name == "c5" else
+                      "reference bench scene (cli.py:239-246), GSPC-rounded"),
             "l2": "flushed between timed steps (256 MiB write)",
             "parallelism": "tx-sharded (independent renders per GPU)"}
 
@@ -233,8 +262,13 @@ def run_ours(args):
 
     n, w, h, F, B = CONFIGS[args.config]
     C = 2 * F
-    cloud = bench_cloud(n, F)
-    dc = DeviceCloud.from_host(cloud)
+    if args.config == "c5":  # 17.6 GB of weights: generated on the device
+        cloud = None
+        dc = device_bench_cloud(n, F)
+        args.no_cpu_baseline = True
+    else:
+        cloud = bench_cloud(n, F)
+        dc = DeviceCloud.from_host(cloud)
     pose = ViewPose(np.zeros(3))
     total_steps = args.steps + args.warmup
     txs_np = sample_tx(1000 + 7919 * rank, total_steps * B)
@@ -360,8 +394,11 @@ def run_ours(args):
             "ms_per_step": ms, "p50_ms": float(np.percentile(times, 50)),
             "p99_ms": float(np.percentile(times, 99)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (reference bench scene recipe, "
-                                    "seeded PCG64; random-init MLP weights)",
+            "dtype": "f32", "data": ("synthetic (bench scene recipe drawn on the device "
+                                     "with torch's generator; random-init MLP weights)"
+                                     if args.config == "c5" else
+                                     "synthetic (reference bench scene recipe, "
+                                     "seeded PCG64; random-init MLP weights)"),
             "config": workload_config(args.config),
             "clocks": clocks.summary(),
             "e2e": {"value": e2e_val, "unit": "renders/s",

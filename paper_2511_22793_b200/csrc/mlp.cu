@@ -101,12 +101,12 @@ __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
   }
 }
 
-// Wide head, f32 weights, H == 16, I == 5, C % 4 == 0, C <= 128.
-// Every load of the Gaussian (its W1/b1 row, all of W2 and b2, theta/phi)
-// is issued before any arithmetic, so one warp has ~7.5 KB in flight and
-// pays a single memory latency per Gaussian.
+// Wide head, f32 weights, H == 16, I == 5, C % 4 == 0.
+// Every load of the Gaussian (its W1/b1 row, W2 and b2, theta/phi) is issued
+// before any arithmetic, so one warp has up to 8 KB in flight and pays one
+// memory latency per 128 output channels (C > 128 streams W2 in parts).
 __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int lane) {
-  constexpr int MAXV = 16;  // 4C/32 float4 per lane (C <= 128)
+  constexpr int MAXV = 16;  // float4 per lane per part: 128 channels
   const float* w = A.w32 + i * (int64_t)A.P;
   const int C = A.C;
   const int nvec = 4 * C;
@@ -118,43 +118,44 @@ __device__ __forceinline__ void mlp_wide_one(const MlpArgs& A, int64_t i, int la
   const float b1 = __ldg(w + 80 + hu);
   const float4* w2v = reinterpret_cast<const float4*>(w + 96);
   const float* b2 = w + 96 + 16 * C;
-  float4 v[MAXV];
-  float bv[MAXV];
-#pragma unroll
-  for (int u = 0; u < MAXV; ++u) {
-    const int f = u * 32 + lane;
-    v[u] = f < nvec ? __ldg(w2v + f) : make_float4(0.f, 0.f, 0.f, 0.f);
-    bv[u] = (f < nvec && (lane & 3) == 0) ? __ldg(b2 + (f >> 2)) : 0.f;
-  }
   const int q = lane & 3;
   const double* pp = A.pos + 3 * i;
   const double pv[3] = {__ldg(pp), __ldg(pp + 1), __ldg(pp + 2)};  // issued with the weights
-  const double* p = pv;
-  for (int b = 0; b < A.B; ++b) {
-    const double* txb = A.tx + 3 * b;
-    float x[5] = {(float)txb[0], (float)txb[1], (float)txb[2], r1.z, r1.w};
-    float pre = 0.f;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) pre += w1[k] * x[k];
-    pre += b1;
-    const float hid = pre > 0.f ? pre : 0.f;
-    const float h0 = __shfl_sync(0xffffffffu, hid, 4 * q + 0);
-    const float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
-    const float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
-    const float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
-    // s / d_tx (rasterizer.py:200): one f64 reciprocal per (Gaussian, TX);
-    // x * (1/d) differs from x / d by <= 1 ulp in f64, invisible after the
-    // cast to f32 except on exact rounding ties
-    const double rd = 1.0 / tx_distance(p, txb);
-    float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+  for (int part = 0; part * MAXV * 32 < nvec; ++part) {
+    float4 v[MAXV];
+    float bv[MAXV];
 #pragma unroll
     for (int u = 0; u < MAXV; ++u) {
-      if (u * 32 >= nvec) break;
-      const int f = u * 32 + lane;
-      float part = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
-      part += __shfl_xor_sync(0xffffffffu, part, 1);
-      part += __shfl_xor_sync(0xffffffffu, part, 2);
-      if (q == 0 && f < nvec) out[f >> 2] = (float)((double)(part + bv[u]) * rd);
+      const int f = (part * MAXV + u) * 32 + lane;
+      v[u] = f < nvec ? __ldg(w2v + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+      bv[u] = (f < nvec && (lane & 3) == 0) ? __ldg(b2 + (f >> 2)) : 0.f;
+    }
+    for (int b = 0; b < A.B; ++b) {
+      const double* txb = A.tx + 3 * b;
+      float x[5] = {(float)txb[0], (float)txb[1], (float)txb[2], r1.z, r1.w};
+      float pre = 0.f;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) pre += w1[k] * x[k];
+      pre += b1;
+      const float hid = pre > 0.f ? pre : 0.f;
+      const float h0 = __shfl_sync(0xffffffffu, hid, 4 * q + 0);
+      const float h1 = __shfl_sync(0xffffffffu, hid, 4 * q + 1);
+      const float h2 = __shfl_sync(0xffffffffu, hid, 4 * q + 2);
+      const float h3 = __shfl_sync(0xffffffffu, hid, 4 * q + 3);
+      // s / d_tx (rasterizer.py:200): one f64 reciprocal per (Gaussian, TX);
+      // x * (1/d) differs from x / d by <= 1 ulp in f64, invisible after the
+      // cast to f32 except on exact rounding ties
+      const double rd = 1.0 / tx_distance(pv, txb);
+      float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+#pragma unroll
+      for (int u = 0; u < MAXV; ++u) {
+        const int f = (part * MAXV + u) * 32 + lane;
+        if ((part * MAXV + u) * 32 >= nvec) break;
+        float acc = v[u].x * h0 + v[u].y * h1 + v[u].z * h2 + v[u].w * h3;
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (q == 0 && f < nvec) out[f >> 2] = (float)((double)(acc + bv[u]) * rd);
+      }
     }
   }
 }
@@ -216,7 +217,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     }
     int64_t threads = cloud.n * B;
     k_mlp_narrow<double><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
-  } else if (A.C % 4 == 0 && A.C >= 16 && A.C <= 128 && A.H == 16 && A.I == 5) {
+  } else if (A.C % 4 == 0 && A.C >= 16 && A.H == 16 && A.I == 5) {
     int64_t threads = cloud.n * 32;
     int64_t blocks = (threads + 255) / 256;
     // live list: one wave (2 CTAs per SM), grid-stride over the list; most
