@@ -160,6 +160,8 @@ typedef struct gsparc_frame_layout {
   int64_t off_det_inv;    /* i32  [n,320] list position of every (Gaussian,
                              tile of its rectangle) in canonical tile order
                              (with_backward == 2; written by K3)          */
+  int64_t off_sort_tmp;   /* u64  [pair_capacity] K3 scratch for tile lists
+                             longer than shared memory                    */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

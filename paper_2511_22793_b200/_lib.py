@@ -54,7 +54,7 @@ class CLayout(ctypes.Structure):
                  ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64),
                  ("off_stage", c_i64), ("off_seg", c_i64), ("seg_stride", c_i64),
                  ("off_pxw", c_i64), ("pxw_chunks", c_i64), ("off_ch_wm", c_i64),
-                 ("off_det_inv", c_i64)])
+                 ("off_det_inv", c_i64), ("off_sort_tmp", c_i64)])
 
 
 class CEmitter(ctypes.Structure):

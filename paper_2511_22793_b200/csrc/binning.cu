@@ -33,6 +33,7 @@ struct SortArgs {
   const int2* seg;
   const uint64_t* stage;
   int64_t seg_stride;
+  uint64_t* sort_tmp;  // [pair_capacity] scratch for lists beyond shared memory
   int* inv;          // deterministic frames: [n][DET_MAXT] list positions
   const int4* rect;  // tile rectangles (K2)
   int ntx;
@@ -132,6 +133,7 @@ constexpr int RS_CAP = RS_T * RS_E;  // 8192 keys per tile in shared memory
 constexpr int BK_BITS = 13;          // bucket pass: top 13 bits of the key
 constexpr int BK_N = 1 << BK_BITS;
 constexpr int BK_BIG = 64;           // larger buckets -> LSD radix fallback
+constexpr int BK_BIG_G = 256;        // long lists: larger buckets -> bitonic fallback
 constexpr int SEG_MAX = 4096;        // staged segments per tile gathered in parallel
 
 __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, int n,
@@ -215,6 +217,72 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
     dst = t;
   }
   return src;  // buffer holding the result
+}
+
+// One bucket pass of K3 on keys a[0..n) (shared or global memory): bcnt holds
+// the BK_N bucket counts on entry; exclusive scan -> bucket starts, scatter
+// a -> b by bucket, then every key is ranked inside its (small) bucket by
+// (coarse32, index) and written back to a in sorted order.  Ends with the
+// CTA's writes to a visible to the CTA.
+__device__ void bucket_pass(uint64_t* a, uint64_t* b, int* bcnt, int* bcur, int n,
+                            uint32_t cmin, int bshift) {
+  // exclusive scan of the bucket counts (BK_N / blockDim per thread)
+  constexpr int PER = BK_N / RS_T;
+  int loc[PER];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    loc[k] = sum;
+    sum += bcnt[threadIdx.x * PER + k];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  __shared__ int s_wsum[RS_W];
+  if (lane == 31) s_wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int x = s_wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += u;
+    }
+    s_wsum[lane] = x;
+  }
+  __syncthreads();
+  const int base0 = inc - sum + (wid > 0 ? s_wsum[wid - 1] : 0);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int st0 = base0 + loc[k];
+    bcur[threadIdx.x * PER + k] = st0;
+    bcnt[threadIdx.x * PER + k] = st0;  // bucket start
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint64_t v = a[j];
+    const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
+    b[atomicAdd(bcur + bk, 1)] = v;
+  }
+  __syncthreads();
+  // every key's rank inside its bucket: one pass over the (small)
+  // bucket per key, all keys in parallel; written to a in sorted order
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint64_t v = b[j];
+    const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
+    const int lo = bcnt[bk], hi = bcur[bk];
+    int rank = lo;
+    for (int i = lo; i < hi; ++i) {
+      const uint64_t u = b[i];
+      rank += (u < v) || (u == v && i < j);  // equal keys: seam duplicates
+    }
+    a[rank] = v;
+  }
+  __syncthreads();
 }
 
 // Gather each tile's staged segments, sort them by (coarse depth, index),
@@ -363,63 +431,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 3] = clock64() - t_dbg0;
     uint64_t* r;
     if (s_bmax < BK_BIG) {
-      // exclusive scan of the bucket counts (BK_N / blockDim per thread)
-      constexpr int PER = BK_N / RS_T;
-      int loc[PER];
-      int sum = 0;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        loc[k] = sum;
-        sum += bcnt[threadIdx.x * PER + k];
-      }
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      int inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
-      }
-      __shared__ int s_wsum[RS_W];
-      if (lane == 31) s_wsum[wid] = inc;
-      __syncthreads();
-      if (wid == 0) {
-        int x = s_wsum[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += u;
-        }
-        s_wsum[lane] = x;
-      }
-      __syncthreads();
-      const int base0 = inc - sum + (wid > 0 ? s_wsum[wid - 1] : 0);
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int st0 = base0 + loc[k];
-        bcur[threadIdx.x * PER + k] = st0;
-        bcnt[threadIdx.x * PER + k] = st0;  // bucket start
-      }
-      __syncthreads();
-      if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 4] = clock64() - t_dbg0;
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const uint64_t v = a[j];
-        const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
-        b[atomicAdd(bcur + bk, 1)] = v;
-      }
-      __syncthreads();
-      // every key's rank inside its bucket: one pass over the (small)
-      // bucket per key, all keys in parallel; written to a in sorted order
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const uint64_t v = b[j];
-        const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
-        const int lo = bcnt[bk], hi = bcur[bk];
-        int rank = lo;
-        for (int i = lo; i < hi; ++i) {
-          const uint64_t u = b[i];
-          rank += (u < v) || (u == v && i < j);  // equal keys: seam duplicates
-        }
-        a[rank] = v;
-      }
+      bucket_pass(a, b, bcnt, bcur, n, cmin, bshift);
       __syncthreads();
       if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 5] = clock64() - t_dbg0;
       r = a;
@@ -436,8 +448,31 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   } else if (n == 1) {
     if (threadIdx.x == 0) g[0] = s_keys[0];
   } else if (n > RS_CAP) {
+    // longer than shared memory: the same bucket pass with the keys in L2
+    // (g and a scratch slice of the same offsets), the counters in shared
+    // memory; a bucket of >= BK_BIG_G keys falls back to a bitonic sort
     if (threadIdx.x == 0) atomicAdd(A.counters + GSPARC_CNT_BIGTILE, 1);
-    bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
+    int* cnt = (int*)(s_keys + 2 * RS_CAP);
+    int* bcnt = cnt;
+    int* bcur = cnt + BK_N;
+    const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
+    const int bits = span ? 32 - __clz(span) : 0;
+    const int bshift = bits > BK_BITS ? bits - BK_BITS : 0;
+    __shared__ int s_gbig;
+    if (threadIdx.x == 0) s_gbig = 0;
+    for (int q = threadIdx.x; q < BK_N; q += blockDim.x) bcnt[q] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const int bk = (int)(((uint32_t)(g[j] >> 32) - cmin) >> bshift);
+      if (atomicAdd(bcnt + bk, 1) == BK_BIG_G) s_gbig = 1;
+    }
+    __syncthreads();
+    if (!s_gbig && A.sort_tmp) {
+      bucket_pass(g, A.sort_tmp + s, bcnt, bcur, n, cmin, bshift);
+    } else {
+      bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
+      __syncthreads();
+    }
     fix_coarse_ties(g, n, A.key);
     __syncthreads();
   }
@@ -469,6 +504,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.stage = (const uint64_t*)(frame + L.off_stage);
   A.seg_stride = L.seg_stride;
   A.inv = L.with_backward == 2 ? (int*)(frame + L.off_det_inv) : nullptr;
+  A.sort_tmp = (uint64_t*)(frame + L.off_sort_tmp);
   A.rect = (const int4*)(frame + L.off_rect);
   A.ntx = L.ntx;
   A.ntiles = L.ntiles;
