@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
     for (int b0 = 0; b0 < A.B; b0 += 32) {
       const int b = b0 + lane;
       const bool vb = b < A.B;
-      double x[I5], hid[H16], gh[H16], pre[H16];
+      double x[I5], hid[H16], gh[H16];
       x[3] = theta;
       x[4] = phi;
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, draw = 1.0, d = 1.0;
@@ -131,7 +131,6 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
 #pragma unroll
         for (int k = 0; k < I5; ++k) v += (double)W1[h * I5 + k] * x[k];
         v += (double)b1[h];
-        pre[h] = v;
         hid[h] = v > 0.0 ? v : 0.0;
         gh[h] = 0.0;
       }
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
       }
 #pragma unroll
       for (int h = 0; h < H16; ++h) {
-        const double gp = pre[h] > 0.0 ? gh[h] : 0.0;
+        const double gp = hid[h] > 0.0 ? gh[h] : 0.0;  // relu' (pre > 0 <=> hid > 0)
         gth += (double)W1[h * I5 + 3] * gp;
         gph += (double)W1[h * I5 + 4] * gp;
         t_gp[lane * (H16 + 1) + h] = gp;
