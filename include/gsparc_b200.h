@@ -72,6 +72,9 @@ enum {
   GSPARC_CNT_LIVE = 3,      /* Gaussians with >= 1 included contribution  */
   GSPARC_CNT_NONFINITE = 4, /* nonzero: non-finite gradient seen by Adam  */
   GSPARC_CNT_BIGTILE = 5,   /* tiles sorted by the out-of-shared-mem path */
+  GSPARC_CNT_SORTED = 6,    /* tiles published to the K3 -> K4a queue     */
+  GSPARC_CNT_CLAIMED = 7,   /* queue entries claimed by pass-A CTAs       */
+  GSPARC_CNT_PXA_DONE = 8,  /* pass-A CTAs whose live-list entries are written */
   GSPARC_NUM_COUNTERS = 16
 };
 
@@ -110,7 +113,7 @@ typedef struct gsparc_frame_layout {
   int64_t off_rect;       /* i32  [n,4] tile rectangle + pair count     */
   int64_t off_counters;   /* i32  [16]                                  */
   int64_t off_tile_count; /* i32  [ntiles] pairs per tile               */
-  int64_t off_tile_cursor;/* i32  [ntiles] reserved (zeroed)             */
+  int64_t off_tile_cursor;/* i32  [ntiles] K3 -> K4a queue: tile + 1 in sort-completion order (zeroed) */
   int64_t off_tile_start; /* i32  [ntiles+1]                            */
   int64_t off_tile_stop;  /* i32  [ntiles*4] list prefix visited per sub-tile */
   int64_t off_pairs;      /* u64  [pair_capacity] per-tile sorted lists */

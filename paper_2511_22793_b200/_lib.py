@@ -17,7 +17,7 @@ ABI_VERSION = 3
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
 F32, F64 = 0, 1
 LAZY_MLP, FORCE_FUSED = 1, 2
-CNT_KEPT, CNT_PAIRS, CNT_OVERFLOW, CNT_LIVE, CNT_NONFINITE, CNT_BIGTILE = range(6)
+CNT_KEPT, CNT_PAIRS, CNT_OVERFLOW, CNT_LIVE, CNT_NONFINITE, CNT_BIGTILE, CNT_SORTED, CNT_CLAIMED, CNT_PXA_DONE = range(9)
 NUM_COUNTERS = 16
 
 c_i32, c_i64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, \

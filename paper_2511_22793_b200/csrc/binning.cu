@@ -21,7 +21,7 @@
 
 namespace gs {
 
-extern long long* gsparc_dbg_ptr;
+long long* dbg_rows(int which);
 
 struct SortArgs {
   uint64_t* pairs;
@@ -29,7 +29,7 @@ struct SortArgs {
   const uint64_t* key;
   int* counters;
   const int* tile_count;
-  const int* tile_cursor;
+  int* ready;  // [ntiles] queue of sorted tiles, tile + 1 (the frame's tile_cursor, zeroed by K2)
   const int2* seg;
   const uint64_t* stage;
   int64_t seg_stride;
@@ -289,6 +289,8 @@ __device__ void bucket_pass(uint64_t* a, uint64_t* b, int* bcnt, int* bcur, int 
 // fix coarse ties by the full f64 key and write the tile's list.
 __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   const long long t_dbg0 = clock64();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
+  pdl_trigger();  // pass A may be scheduled now; it waits on A.ready per tile
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
   __shared__ int s_start[2];
   __shared__ int s_pos;
@@ -490,6 +492,18 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       if (slot >= 0 && slot < DET_MAXT) A.inv[(int64_t)idx * DET_MAXT + slot] = s + j;
     }
   }
+  // publish the tile: its bounds (same values CTA 0 wrote) and list, then
+  // its id in the next slot of the K3 -> K4a queue (pass A's CTAs take
+  // tiles in the order their sorts finish)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    A.tile_start[t] = s;
+    A.tile_start[t + 1] = s + n;
+    __threadfence();
+    const int q = atomicAdd(A.counters + GSPARC_CNT_SORTED, 1);
+    flag_release(A.ready + q, t + 1);
+  }
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 15] = gtimer();
 }
 
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
@@ -499,7 +513,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.key = (const uint64_t*)(frame + L.off_key);
   A.counters = (int*)(frame + L.off_counters);
   A.tile_count = (const int*)(frame + L.off_tile_count);
-  A.tile_cursor = (const int*)(frame + L.off_tile_cursor);
+  A.ready = (int*)(frame + L.off_tile_cursor);
   A.seg = (const int2*)(frame + L.off_seg);
   A.stage = (const uint64_t*)(frame + L.off_stage);
   A.seg_stride = L.seg_stride;
@@ -509,13 +523,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
   A.ntx = L.ntx;
   A.ntiles = L.ntiles;
   A.dbg = nullptr;
-  if (getenv("GSPARC_SORT_DBG")) {  // experiments only
-    static long long* dbg = nullptr;
-    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * 4096);
-    cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * 4096, st);
-    A.dbg = dbg;
-    gsparc_dbg_ptr = dbg;
-  }
+  if (getenv("GSPARC_SORT_DBG")) A.dbg = dbg_rows(0);  // experiments only
   const size_t cnt_ints =
       (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + RS_W + 2 + 3 * SEG_MAX + 1);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;

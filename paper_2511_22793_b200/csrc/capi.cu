@@ -253,7 +253,9 @@ int gsparc_render_forward(const gsparc_cloud* cloud, const gsparc_view* view,
   const bool lazy = (flags & GSPARC_LAZY_MLP) && !(flags & GSPARC_FORCE_FUSED);
   if (lazy) {
     GS_TRY(launch_raster_forward(*L, f, n_tx, cloud->mlp_out, t_eps, 1, image_out, st));
-    GS_TRY(launch_mlp(*cloud, tx_dev, n_tx, true, *L, f, st));
+    // f32 frames: the MLP streams the live list while pass A finishes
+    const int stream_ctas = L->dtype == GSPARC_F32 ? 2 * (int)L->ntiles : 0;
+    GS_TRY(launch_mlp(*cloud, tx_dev, n_tx, true, *L, f, st, stream_ctas));
     return launch_raster_forward(*L, f, n_tx, cloud->mlp_out, t_eps, 2, image_out, st);
   }
   GS_TRY(launch_mlp(*cloud, tx_dev, n_tx, false, *L, f, st));

@@ -290,6 +290,29 @@ __device__ __forceinline__ double warp_sum(double v) {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 
+// experiments: global nanosecond timer (per-CTA timelines in the dbg buffers)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Programmatic dependent launch (K3 -> K4a): the sort lets pass A's CTAs be
+// scheduled as soon as it is resident; pass A waits per tile on a release
+// flag instead of on the whole sort grid.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void flag_release(int* f, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(const int* f) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+
 }  // namespace gs
 
 #define GS_TRY(expr)                       \

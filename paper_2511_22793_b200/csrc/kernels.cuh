@@ -11,7 +11,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
                       const gsparc_frame_layout& L, char* frame, cudaStream_t st);
 int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st);
 int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_only,
-               const gsparc_frame_layout& L, char* frame, cudaStream_t st);
+               const gsparc_frame_layout& L, char* frame, cudaStream_t st, int stream_ctas = 0);
 int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                           double t_eps, int pass, void* img, cudaStream_t st);
 int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C, double t_eps,

@@ -11,6 +11,8 @@
 //           loads (lane l reads float4 #l of the row block), partial dots
 //           reduced over the 4 lanes that share an output row.  This is the
 //           HBM-bound path of the 52-subcarrier config (7.5 KB per Gaussian).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -28,6 +30,7 @@ struct MlpArgs {
   const int* counters;
   void* coef;
   int64_t n;
+  int stream_ctas;  // > 0: started during pass A (PDL); entries appear as its CTAs finish
   int B, C, H, I, P;
   int64_t Cp;  // B*C
 };
@@ -164,6 +167,29 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (A.live_list && A.stream_ctas) {
+    // streaming: the list is -1 where pass A has not written yet (K2 clears
+    // it); a warp takes entries wid, wid + nwarps, ... as they appear, and
+    // stops at the first empty entry once every pass-A CTA has finished
+    for (int64_t gi = wid; gi < A.n; gi += nwarps) {
+      int v = __ldcv(A.live_list + gi);
+      long long spins = 0;
+      while (v < 0) {
+        if (flag_acquire(A.counters + GSPARC_CNT_PXA_DONE) >= A.stream_ctas ||
+            __ldcv(A.counters + GSPARC_CNT_OVERFLOW)) {
+          v = __ldcv(A.live_list + gi);
+          break;
+        }
+        __nanosleep(256);
+        if (++spins > (1ll << 22)) break;  // bounded (pass A never ran): leave
+        v = __ldcv(A.live_list + gi);
+      }
+      if (v < 0) break;
+      mlp_wide_one(A, v, lane);
+    }
+    pdl_wait();  // complete only after pass A has
+    return;
+  }
   if (A.live_list) {  // one warp per live Gaussian, all in flight
     // the list entry is read speculatively together with the count (the
     // list has room for n entries), saving one dependent round trip
@@ -180,8 +206,9 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
 }
 
 int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_only,
-               const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
+               const gsparc_frame_layout& L, char* frame, cudaStream_t st, int stream_ctas) {
   MlpArgs A;
+  A.stream_ctas = 0;
   A.w32 = cloud.mlp_weights;
   A.w64 = cloud.mlp_weights64;
   A.pos = cloud.positions;
@@ -223,7 +250,23 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     // live list: one wave (2 CTAs per SM), grid-stride over the list; most
     // renders have fewer live Gaussians than resident warps
     if (live_only && blocks > 148 * 2) blocks = 148 * 2;
-    k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
+    if (live_only && stream_ctas > 0 && !getenv("GSPARC_NO_PDL")) {
+      // programmatic dependent launch behind pass A (which triggers at its
+      // start): the MLP runs while pass A's last CTAs finish
+      A.stream_ctas = stream_ctas;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      cfg.gridDim = dim3((unsigned)blocks);
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_mlp_wide, A);
+    } else {
+      k_mlp_wide<<<(unsigned)blocks, 256, 0, st>>>(A);
+    }
   } else {
     int64_t threads = cloud.n * B;
     k_mlp_narrow<float><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);

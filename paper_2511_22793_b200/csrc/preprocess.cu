@@ -21,6 +21,7 @@ struct PrepArgs {
   float4* rrec;
   int4* rect;
   int* live;
+  int* live_list;
   int* counters;
   int* tile_count;
   int* tile_cursor;
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
       r[7] = phi;
     }
     A.live[i] = 0;  // K4 pass A flags the Gaussians with a contribution
+    A.live_list[i] = -1;  // entries appear as pass A appends them (streaming K1)
     A.rect[i] = make_int4(y0 | (y1 << 16), (a0 & 0xffff) | (a1 << 16), (b0 & 0xffff) | (b1 << 16),
                           npairs);
     if (keep) {
@@ -351,6 +353,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.tile_count = (int*)(frame + L.off_tile_count);
   A.tile_cursor = (int*)(frame + L.off_tile_cursor);
   A.live = (int*)(frame + L.off_live);
+  A.live_list = (int*)(frame + L.off_live_list);
   A.stage = (uint64_t*)(frame + L.off_stage);
   A.seg = (int2*)(frame + L.off_seg);
   A.capacity = L.pair_capacity;

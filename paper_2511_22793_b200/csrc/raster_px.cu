@@ -60,6 +60,7 @@ struct PxArgs {
   float* img;
   float4* pxw;    // [2*ntiles][wmax][8][128] weights of the first wmax chunks
   uint32_t* ch_wm;  // [slots][4] per-warp included-entry mask
+  const int* ready;  // pass A: K3's per-tile flags (null: the sort grid has completed)
   int wmax;
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
@@ -155,10 +156,37 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const long long t_startA = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const CtaGeom g = cta_geom(A, blockIdx.x);
-  const int start = A.tile_start[g.tile];
-  const int len = A.tile_start[g.tile + 1] - start;
-  const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
+  int cta = blockIdx.x;  // (tile, half) = (cta >> 1, cta & 1)
+  if (A.ready) {
+    // launched while K3 runs: claim the next (tile, half) in the order the
+    // sorts finished and wait until it is published (bounded: a frame whose
+    // sort never ran reports an error instead of hanging)
+    __shared__ int s_cta;
+    if (threadIdx.x == 0) {
+      const int h = atomicAdd(A.counters + GSPARC_CNT_CLAIMED, 1) % (2 * A.ntiles);
+      long long spins = 0;
+      int v;
+      while (!(v = flag_acquire(A.ready + (h >> 1)))) {
+        __nanosleep(64);
+        if (++spins > (1ll << 24)) {
+          atomicExch(A.counters + GSPARC_CNT_OVERFLOW, 2);
+          v = (h >> 1) + 1;
+          break;
+        }
+      }
+      s_cta = 2 * (v - 1) + (h & 1);
+    }
+    __syncthreads();
+    cta = s_cta;
+  }
+  if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 14] = gtimer();
+  pdl_trigger();  // the lazy MLP (K1) may start and consume the live list as it grows
+  const CtaGeom g = cta_geom(A, cta);
+  // the tile's bounds and list were written by a grid that may still be
+  // running: read them through L2
+  const int start = __ldcg(A.tile_start + g.tile);
+  const int len = __ldcg(A.tile_start + g.tile + 1) - start;
+  const int64_t slot0 = 2 * ((start + 31 * (int64_t)g.tile) >> 5) + g.half * ((len + 31) >> 5);
   if (threadIdx.x == 0) {
     for (int s = 0; s < PX_RING; ++s) {
       mbar_init(&s_full[s], 1);
@@ -197,7 +225,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     // ahead (the record load depends on the index load)
     constexpr int DI = 6, DR = 3;
     auto ld_idx = [&](int p) -> uint32_t {
-      return p + lane < end ? (uint32_t)__ldg(A.pairs + start + p + lane) : 0xffffffffu;
+      return p + lane < end ? (uint32_t)__ldcg(A.pairs + start + p + lane) : 0xffffffffu;
     };
     auto ld_rec = [&](uint32_t i, float4& a, float4& b) {
       if (i != 0xffffffffu) {
@@ -280,9 +308,9 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     acquire(c);
     publish(c, -1);  // end of list
     if (A.dbg && lane == 0) {
-      A.dbg[blockIdx.x * 16 + 0] = tpe;
-      A.dbg[blockIdx.x * 16 + 1] = clock64() - t_startA;
-      A.dbg[blockIdx.x * 16 + 2] = c;
+      A.dbg[cta * 16 + 0] = tpe;
+      A.dbg[cta * 16 + 1] = clock64() - t_startA;
+      A.dbg[cta * 16 + 2] = c;
     }
   } else {
     // ---------------- consumers: one pixel per lane
@@ -310,7 +338,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       // the pixel's 32 blending weights of this chunk, stored for pass B
       // (coalesced: entry quad j of the CTA's 128 pixels is one 2 KB row)
       const bool wst = !SC && c < A.wmax;
-      float4* wrow = A.pxw + ((int64_t)blockIdx.x * A.wmax + c) * 8 * 128 + warp * 32 + lane;
+      float4* wrow = A.pxw + ((int64_t)cta * A.wmax + c) * 8 * 128 + warp * 32 + lane;
       unsigned um = 0;
       if (!wdone) {
         unsigned actm = 0;
@@ -358,8 +386,8 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       if (lane == 0) mbar_arrive(&s_empty[s]);
     }
     if (A.dbg && lane == 0) {
-      A.dbg[blockIdx.x * 16 + 3 + warp] = twf;
-      A.dbg[blockIdx.x * 16 + 7 + warp] = tcc;
+      A.dbg[cta * 16 + 3 + warp] = twf;
+      A.dbg[cta * 16 + 7 + warp] = tcc;
     }
     if (inside) {
       const int q = py * A.w + px;
@@ -381,10 +409,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) A.ch_n[blockIdx.x] = s_nch;
+  if (threadIdx.x == 0) A.ch_n[cta] = s_nch;
   if (A.dbg && threadIdx.x == 0) {
-    A.dbg[blockIdx.x * 16 + 11] = clock64() - t_startA;
-    A.dbg[blockIdx.x * 16 + 12] = s_nch;
+    A.dbg[cta * 16 + 11] = clock64() - t_startA;
+    A.dbg[cta * 16 + 12] = s_nch;
   }
   // live list (for the lazy MLP): entries of this CTA's chunks with an
   // included contribution; the first CTA to flag a Gaussian appends it.
@@ -398,6 +426,17 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       if (atomicExch(A.live + idx, 1) == 0) A.live_list[atomicAdd(A.counters + GSPARC_CNT_LIVE, 1)] = idx;
     }
   }
+  // this CTA's live-list entries are written: count it finished (K1 stops
+  // waiting for entries once every pass-A CTA has)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(A.counters + GSPARC_CNT_PXA_DONE, 1);
+  }
+  if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 15] = gtimer();
+  // this grid completes only after K3 has (its writes are then visible to
+  // every later kernel in the stream)
+  if (A.ready) pdl_wait();
 }
 
 // ------------------------------------------------------------------ pass B
@@ -496,6 +535,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
 
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const long long t_start = clock64();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 12] = gtimer();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CtaGeom g = cta_geom(A, blockIdx.x);
   const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
@@ -818,10 +858,22 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   if (A.dbg && threadIdx.x == 0) {
     A.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
     A.dbg[blockIdx.x * 16 + 11] = nch;
+    A.dbg[blockIdx.x * 16 + 15] = gtimer();
   }
 }
 
-long long* gsparc_dbg_ptr = nullptr;  // experiments: last pass-B timing buffer
+long long* gsparc_dbg_ptr = nullptr;  // experiments: timing rows (K3 | K4a | K4b)
+
+// experiments: one buffer of 16-slot rows: K3 rows [0, 4096), K4a rows
+// [4096, 8192), K4b rows [8192, 12288); cleared once (a per-launch memset
+// would split the K3 -> K4a programmatic launch)
+long long* dbg_rows(int which) {
+  if (!gsparc_dbg_ptr) {
+    cudaMalloc(&gsparc_dbg_ptr, sizeof(long long) * 16 * 12288);
+    cudaMemset(gsparc_dbg_ptr, 0, sizeof(long long) * 16 * 12288);
+  }
+  return gsparc_dbg_ptr + (int64_t)which * 16 * 4096;
+}
 
 template <int NP>
 static void launch_pxb(const PxArgs& A, int chunks_y, cudaStream_t st) {
@@ -839,13 +891,7 @@ static void launch_pxb(const PxArgs& A, int chunks_y, cudaStream_t st) {
   }
   PxArgs B = A;
   B.dbg = nullptr;
-  static long long* dbg = nullptr;
-  if (getenv("GSPARC_PXB_DBG")) {  // experiments only
-    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 16 * 4096);
-    cudaMemsetAsync(dbg, 0, sizeof(long long) * 16 * 4096, st);
-    B.dbg = dbg;
-    gsparc_dbg_ptr = dbg;
-  }
+  if (getenv("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   k_pxb<NP><<<dim3(A.ntiles * 2, chunks_y), CF::THREADS, smem, st>>>(B);
 }
 
@@ -873,6 +919,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.pxw = (float4*)(frame + L.off_pxw);
   A.ch_wm = (uint32_t*)(frame + L.off_ch_wm);
   A.wmax = (int)L.pxw_chunks;
+  A.ready = nullptr;
   A.Cp = (int64_t)n_tx * C;
   A.n = L.n;
   A.C = C;
@@ -894,25 +941,59 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
   PxArgs A = make_px_args(L, frame, n_tx, C, t_eps, img);
   const int64_t Cp = A.Cp;
   if (pass != 2 && getenv("GSPARC_PXA_DBG")) {  // experiments only: pass-A timing
-    static long long* dbga = nullptr;
-    if (!dbga) cudaMalloc(&dbga, sizeof(long long) * 16 * 4096);
-    cudaMemsetAsync(dbga, 0, sizeof(long long) * 16 * 4096, st);
-    A.dbg = dbga;
-    gsparc_dbg_ptr = dbga;
+    A.dbg = dbg_rows(1);
   }
   if (pass != 2) {
     const int grid = L.ntiles * 2;
+    // programmatic dependent launch: pass A's CTAs start while K3 (the
+    // stream's previous kernel, which triggers at its start) still sorts
+    // other tiles; each waits for its own tile's flag.  If the previous
+    // kernel is not K3 the launch degrades to ordinary stream order and the
+    // flags (set by the frame's K3) are already up.
+    static const bool pdl = !getenv("GSPARC_NO_PDL");
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(160);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    // two pass-A CTAs per SM at most (a shared-memory reservation): CTAs
+    // that start while K3 still runs would otherwise pile up four to an SM
+    // on the first free SMs and run the heaviest tiles at half speed
+    static const int pad_kb = getenv("GSPARC_PXA_SMEM") ? atoi(getenv("GSPARC_PXA_SMEM")) : 90;
+    if (pdl && pad_kb > 0) {
+      static bool attr = false;
+      if (!attr) {
+        const void* ks[5] = {(const void*)k_pxa<0>, (const void*)k_pxa<1>, (const void*)k_pxa<2>,
+                             (const void*)k_pxa<3>, (const void*)k_pxa<4>};
+        for (const void* k : ks) {
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_kb * 1024);
+          cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+        }
+        attr = true;
+      }
+      cfg.dynamicSmemBytes = pad_kb * 1024;
+    }
+    if (pdl) {
+      A.ready = (const int*)(frame + L.off_tile_cursor);
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
     if (pass == 0 && Cp <= 4) {
       switch (Cp) {
-        case 1: k_pxa<1><<<grid, 160, 0, st>>>(A); break;
-        case 2: k_pxa<2><<<grid, 160, 0, st>>>(A); break;
-        case 3: k_pxa<3><<<grid, 160, 0, st>>>(A); break;
-        default: k_pxa<4><<<grid, 160, 0, st>>>(A); break;
+        case 1: cudaLaunchKernelEx(&cfg, k_pxa<1>, A); break;
+        case 2: cudaLaunchKernelEx(&cfg, k_pxa<2>, A); break;
+        case 3: cudaLaunchKernelEx(&cfg, k_pxa<3>, A); break;
+        default: cudaLaunchKernelEx(&cfg, k_pxa<4>, A); break;
       }
       return check_launch("k_pxa");
     }
-    k_pxa<0><<<grid, 160, 0, st>>>(A);
+    cudaLaunchKernelEx(&cfg, k_pxa<0>, A);
     GS_TRY(check_launch("k_pxa"));
+    A.ready = nullptr;
     if (pass == 1) return GSPARC_OK;
   }
   const int chunks = (int)((Cp + 255) / 256);

@@ -16,9 +16,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 L = _lib.lib()
 n = 276
-host = (ctypes.c_longlong * (n * 16))()
-assert L.gsparc_debug_copy(host, ctypes.c_int64(n * 16)) == 0
-d = np.ctypeslib.as_array(host).reshape(n, 16)
+host = (ctypes.c_longlong * (12288 * 16))()
+assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
+d = np.ctypeslib.as_array(host).reshape(12288, 16)[1 * 4096:1 * 4096 + n]
 names = ["prod_wait_empty", "prod_total", "prod_chunks", "w0_wait_full", "w1_wait_full",
          "w2_wait_full", "w3_wait_full", "w0_comp", "w1_comp", "w2_comp", "w3_comp",
          "total", "nch"]

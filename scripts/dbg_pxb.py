@@ -16,9 +16,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 L = _lib.lib()
 n = 276
-host = (ctypes.c_longlong * (n * 16))()
-assert L.gsparc_debug_copy(host, ctypes.c_int64(n * 16)) == 0
-d = np.ctypeslib.as_array(host).reshape(n, 16)
+host = (ctypes.c_longlong * (12288 * 16))()
+assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
+d = np.ctypeslib.as_array(host).reshape(12288, 16)[2 * 4096:2 * 4096 + n]
 names = ["mma_wait", "", "", "", "", "", "w0_waitE", "w1_waitE", "w0_comp", "w1_comp",
          "total", "nch", "", "t_prologue_end", "t_epilogue_start"]
 order = np.argsort(-d[:, 10])

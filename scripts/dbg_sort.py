@@ -15,9 +15,9 @@ for _ in range(3):
 torch.cuda.synchronize()
 L = _lib.lib()
 n = 138
-host = (ctypes.c_longlong * (n * 16))()
-assert L.gsparc_debug_copy(host, ctypes.c_int64(n * 16)) == 0
-d = np.ctypeslib.as_array(host).reshape(n, 16)[:, :10]
+host = (ctypes.c_longlong * (12288 * 16))()
+assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
+d = np.ctypeslib.as_array(host).reshape(12288, 16)[0 * 4096:0 * 4096 + n][:, :10]
 ts = frame.view("tile_start", torch.int32, (n + 1,)).cpu().numpy()
 ln = np.diff(ts)
 print("phase ends: prologue gather hist scan+scatter rank - ties+write | seg-scan search+load-issue")

@@ -1,0 +1,42 @@
+"""Per-CTA timeline of one config-3 render (experiments): globaltimer
+start/end stamps of K3 (per tile), K4a and K4b (per half-tile CTA) from the
+same render, list lengths and pass A's chunks with contributions."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+for e in ("GSPARC_SORT_DBG", "GSPARC_PXA_DBG", "GSPARC_PXB_DBG"):
+    os.environ[e] = "1"
+import numpy as np, torch
+import bench
+from paper_2511_22793_b200 import DeviceCloud, ViewPose, _lib
+from paper_2511_22793_b200.engine import Renderer
+cloud = bench.bench_cloud(50000, 52)
+dc = DeviceCloud.from_host(cloud)
+R = Renderer()
+tx = torch.as_tensor(bench.sample_tx(1000, 1), device="cuda")
+L = _lib.lib()
+for _ in range(5):
+    img, frame = R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=True)
+torch.cuda.synchronize()
+host = (ctypes.c_longlong * (12288 * 16))()
+assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
+D = np.ctypeslib.as_array(host).reshape(3, 4096, 16)
+nt = 138
+ds, da, db = D[0, :nt], D[1, :2 * nt], D[2, :2 * nt]
+ts = frame.view("tile_start", torch.int32, (nt + 1,)).cpu().numpy()
+ln = np.diff(ts)
+t0 = ds[:, 14].min()
+us = lambda v: (v - t0) / 1e3
+s0, s1 = us(ds[:, 14]), us(ds[:, 15])
+a0, a1 = us(da[:, 14]), us(da[:, 15])
+b0, b1 = us(db[:, 12]), us(db[:, 15])
+print("times in us from the first K3 CTA start")
+print("K3  start %.1f..%.1f end max %.1f mean %.1f" % (s0.min(), s0.max(), s1.max(), s1.mean()))
+print("K4a start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (a0.min(), a0.max(), a1.max(), (a1 - a0).max(), (a1 - a0).mean()))
+print("K4b start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (b0.min(), b0.max(), b1.max(), (b1 - b0).max(), (b1 - b0).mean()))
+wait = a0 - np.repeat(s1, 2)
+print("pass A start - own sort end: min %.1f max %.1f mean %.1f" % (wait.min(), wait.max(), wait.mean()))
+print("tile len  sort[s,e]  passA[s,e]x2  nch  passB dur")
+for t in np.argsort(-np.maximum(a1[0::2], a1[1::2]))[:12]:
+    print(t, ln[t], "[%.1f %.1f]" % (s0[t], s1[t]),
+          "[%.1f %.1f] [%.1f %.1f]" % (a0[2 * t], a1[2 * t], a0[2 * t + 1], a1[2 * t + 1]),
+          da[2 * t:2 * t + 2, 12], ((db[2 * t:2 * t + 2, 15] - db[2 * t:2 * t + 2, 12]) / 1e3).round(1))
