@@ -250,7 +250,12 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     // live list: one wave (2 CTAs per SM), grid-stride over the list; most
     // renders have fewer live Gaussians than resident warps
     if (live_only && blocks > 148 * 2) blocks = 148 * 2;
+    static const int stream_blocks =
+        getenv("GSPARC_MLP_SBLOCKS") ? atoi(getenv("GSPARC_MLP_SBLOCKS")) : 148;
     if (live_only && stream_ctas > 0 && !getenv("GSPARC_NO_PDL")) {
+      // one CTA per SM: all resident next to pass A's two CTAs, so no entry
+      // waits for a CTA that can only start when pass A leaves
+      if (stream_blocks > 0 && blocks > stream_blocks) blocks = stream_blocks;
       // programmatic dependent launch behind pass A (which triggers at its
       // start): the MLP runs while pass A's last CTAs finish
       A.stream_ctas = stream_ctas;

@@ -5,11 +5,14 @@
 // round-to-nearest intrinsics in numpy's evaluation order so the depth key
 // (and therefore the sort order) is bit-identical to numpy's.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace gs {
+
+long long* dbg_rows(int which);
 
 struct PrepArgs {
   gsparc_cloud cloud;
@@ -29,6 +32,7 @@ struct PrepArgs {
   int2* seg;
   int64_t capacity;
   int seg_stride;
+  long long* dbg;  // experiments: per-CTA phase clocks (GSPARC_PREP_DBG)
 };
 
 __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, double b0, double b1,
@@ -50,14 +54,18 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   int* s_off = s_tiles + ntiles;
   int* s_tmp = s_off + ntiles + 1;
   __shared__ int s_base;
+  const long long t_d0 = clock64();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
   __syncthreads();
 
   // Two warps per 32 Gaussians: the even warp runs the view-dependent
-  // chain (projection, pole clamp, J), the odd warp the covariance chain
-  // (quaternion, scales, V = W Sigma W^T) and the opacity, concurrently; the
-  // odd warp's results reach the even warp through shared memory (exact),
-  // which finishes cov2d, the tile rectangle and the records.  Twice the
+  // chain (projection, pole clamp, J) and the opacity with the raster
+  // record's logs, the odd warp the covariance chain (quaternion, scales,
+  // V = W Sigma W^T) and the MLP's elevation input, concurrently (the two
+  // chains measured 7.2k / 6.8k cycles); the odd warp's results reach the
+  // even warp through shared memory (exact), which finishes cov2d, the tile
+  // rectangle and the records.  Twice the
   // warps and half the dependent f64 chain per thread of a
   // one-thread-per-Gaussian mapping, with no divergence inside a warp.
   __shared__ double s_cov[PREP_T / 64][10][32];
@@ -73,7 +81,8 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   double J00 = 0, J02 = 0, J10 = 0, J11 = 0, J12 = 0;
   bool keep = false;
   double V[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-  double opac = 0;
+  double opac = 0, phi = 0, Q = -1.0;
+  float log2op = 0.f;
   if (valid && !cov_lane) {
     const double* P = A.cloud.positions + 3 * i;
     double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
@@ -121,6 +130,20 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     J11 = mul(ce, rho) / jr2;
     J12 = mul(mul(-ce, jy), jz) / r2rho;
 
+    // opacity and the raster record's logs: the view chain is the shorter
+    // of the two, so these run here, ahead of the exchange
+    const double logit = A.cloud.raw_opacities[i];
+    if (logit >= 0.0) {
+      opac = 1.0 / (1.0 + exp(-logit));
+    } else {
+      double e = exp(logit);
+      opac = e / (1.0 + e);
+    }
+    if (A.rrec) {
+      log2op = (float)log2(opac);
+      const double o255 = 255.0 * opac;
+      Q = o255 > 1.0 ? 2.0 * log(o255) : -1.0;
+    }
   }
   if (valid && cov_lane) {
     // Sigma = (R diag s)(R diag s)^T (scene.py:84-88, 117-139)
@@ -167,28 +190,32 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
       for (int c = 0; c < 3; ++c)
         V[r][c] = add(add(mul(WS[r][0], W[3 * c + 0]), mul(WS[r][1], W[3 * c + 1])),
                       mul(WS[r][2], W[3 * c + 2]));
-    const double logit = A.cloud.raw_opacities[i];
-    if (logit >= 0.0) {
-      opac = 1.0 / (1.0 + exp(-logit));
-    } else {
-      double e = exp(logit);
-      opac = e / (1.0 + e);
-    }
+    // the MLP's elevation input (mlp.py:88, unclamped) from the view-space
+    // position, recomputed here with the view chain's operations
+    const double* P = A.cloud.positions + 3 * i;
+    const double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
+                 p2 = sub(P[2], A.pose.rx[2]);
+    const double vx = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
+    const double vy = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
+    const double vz = dot3_seq(p0, p1, p2, W[6], W[7], W[8]);
+    phi = atan2(vy, __dsqrt_rn(add(mul(vx, vx), mul(vz, vz))));
   }
+  if (A.dbg && lane == 0) A.dbg[blockIdx.x * 16 + wid] = clock64() - t_d0;  // chains done
   if (cov_lane) {
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) s_cov[wid >> 1][3 * r + c][lane] = V[r][c];
-    s_cov[wid >> 1][9][lane] = opac;
+    s_cov[wid >> 1][9][lane] = phi;
   }
   __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 8] = clock64() - t_d0;
   if (!cov_lane) {
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int c = 0; c < 3; ++c) V[r][c] = s_cov[wid >> 1][3 * r + c][lane];
-    opac = s_cov[wid >> 1][9][lane];
+    phi = s_cov[wid >> 1][9][lane];
   }
   if (valid && !cov_lane) {
     // cov2d = J V J^T (rasterizer.py:92-95), J row 0 has J01 = 0
@@ -210,7 +237,6 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     double rxr = mul(FOOTPRINT_SIGMA, __dsqrt_rn(a));
     keep = keep && (add(my, ry) >= 0.0) && (sub(my, ry) <= (double)A.gc.h);
 
-    double phi = atan2(y, __dsqrt_rn(rho2_u));  // mlp.py:88 (unclamped)
 
     // tile rectangle (rasterizer.py:117-141)
     const int ntx = A.gc.ntx, nty = A.gc.nty;
@@ -256,9 +282,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     if (A.rrec) {  // f32 raster record (common.cuh "f32 raster alpha")
       const double ca_ = c / det, cb_ = -b / det, cc_ = a / det;
       float xr = -1.f, yr = -1.f;
-      const double o255 = 255.0 * opac;
-      if (o255 > 1.0) {
-        const double Q = 2.0 * log(o255);
+      if (Q > 0.0) {  // 255 opacity > 1
         xr = (float)(sqrt(Q * a) * (1.0 + 1e-4) + 0.01);
         yr = (float)(sqrt(Q * fmax(c, 0.0)) * (1.0 + 1e-4) + 0.01);
       }
@@ -266,7 +290,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
                                   (float)(-LOG2E * cb_));
       // opacity enters the f32 raster as log2(opacity), folded into the
       // exponent: alpha_raw = 2^(q' + log2 opacity)
-      A.rrec[2 * i + 1] = make_float4((float)(-0.5 * LOG2E * cc_), (float)log2(opac), xr, yr);
+      A.rrec[2 * i + 1] = make_float4((float)(-0.5 * LOG2E * cc_), log2op, xr, yr);
     }
     if (A.rec64) {
       double* r = A.rec64 + 8 * i;
@@ -303,7 +327,9 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     if ((threadIdx.x & 31) == 0 && kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
   }
   __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_d0;  // rect+hist
   block_exclusive_scan(s_tiles, s_off, ntiles, s_tmp);  // ends with a barrier
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 10] = clock64() - t_d0;
   const int total = s_off[ntiles];
   if (threadIdx.x == 0) {
     const int base = total ? atomicAdd(A.counters + GSPARC_CNT_PAIRS, total) : 0;
@@ -322,6 +348,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     s_off[t] += base;
   }
   __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 11] = clock64() - t_d0;
   if (kept_out && fits) {
     const int ntx = A.gc.ntx;
     for (int ty = ry0; ty <= ry1; ++ty) {
@@ -333,6 +360,13 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
         const int t = ty * ntx + tx;
         A.stage[atomicAdd(s_off + t, 1)] = packed;
       }
+    }
+  }
+  if (A.dbg) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      A.dbg[blockIdx.x * 16 + 12] = clock64() - t_d0;
+      A.dbg[blockIdx.x * 16 + 15] = gtimer();
     }
   }
 }
@@ -358,6 +392,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.seg = (int2*)(frame + L.off_seg);
   A.capacity = L.pair_capacity;
   A.seg_stride = (int)L.seg_stride;
+  A.dbg = getenv("GSPARC_PREP_DBG") ? dbg_rows(3) : nullptr;  // experiments only
   // counters | tile_count | tile_cursor are laid out back to back
   const int64_t zero_end = L.off_tile_cursor + (int64_t)sizeof(int) * L.ntiles;
   if (L.off_tile_count < L.off_counters || L.off_tile_cursor < L.off_tile_count) {

@@ -865,12 +865,12 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
 long long* gsparc_dbg_ptr = nullptr;  // experiments: timing rows (K3 | K4a | K4b)
 
 // experiments: one buffer of 16-slot rows: K3 rows [0, 4096), K4a rows
-// [4096, 8192), K4b rows [8192, 12288); cleared once (a per-launch memset
+// [4096, 8192), K4b rows [8192, 12288), K2 rows [12288, 16384); cleared once (a per-launch memset
 // would split the K3 -> K4a programmatic launch)
 long long* dbg_rows(int which) {
   if (!gsparc_dbg_ptr) {
-    cudaMalloc(&gsparc_dbg_ptr, sizeof(long long) * 16 * 12288);
-    cudaMemset(gsparc_dbg_ptr, 0, sizeof(long long) * 16 * 12288);
+    cudaMalloc(&gsparc_dbg_ptr, sizeof(long long) * 16 * 16384);
+    cudaMemset(gsparc_dbg_ptr, 0, sizeof(long long) * 16 * 16384);
   }
   return gsparc_dbg_ptr + (int64_t)which * 16 * 4096;
 }
@@ -966,10 +966,11 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
       if (!attr) {
         const void* ks[5] = {(const void*)k_pxa<0>, (const void*)k_pxa<1>, (const void*)k_pxa<2>,
                              (const void*)k_pxa<3>, (const void*)k_pxa<4>};
+        static const int carve =
+            getenv("GSPARC_PXA_CARVE") ? atoi(getenv("GSPARC_PXA_CARVE")) : 100;
         for (const void* k : ks) {
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_kb * 1024);
-          cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
+          cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         }
         attr = true;
       }
