@@ -85,8 +85,11 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   float log2op = 0.f;
   if (valid && !cov_lane) {
     const double* P = A.cloud.positions + 3 * i;
-    double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
-           p2 = sub(P[2], A.pose.rx[2]);
+    // every input load first: a load behind the f64 chain would be a second
+    // DRAM round trip on a cold cache
+    const double logit = __ldg(A.cloud.raw_opacities + i);
+    double p0 = sub(__ldg(P), A.pose.rx[0]), p1 = sub(__ldg(P + 1), A.pose.rx[1]),
+           p2 = sub(__ldg(P + 2), A.pose.rx[2]);
     // (p - rx) @ W.T  (geometry.py:61-64)
     x = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
     y = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
@@ -132,7 +135,6 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
 
     // opacity and the raster record's logs: the view chain is the shorter
     // of the two, so these run here, ahead of the exchange
-    const double logit = A.cloud.raw_opacities[i];
     if (logit >= 0.0) {
       opac = 1.0 / (1.0 + exp(-logit));
     } else {
@@ -147,7 +149,12 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   }
   if (valid && cov_lane) {
     // Sigma = (R diag s)(R diag s)^T (scene.py:84-88, 117-139)
-    const double* q = A.cloud.rotations + 4 * i;
+    const double* P = A.cloud.positions + 3 * i;
+    const double P0 = __ldg(P), P1 = __ldg(P + 1), P2 = __ldg(P + 2);  // loads first
+    const double* qp = A.cloud.rotations + 4 * i;
+    const double* lsp = A.cloud.log_scales + 3 * i;
+    const double q[4] = {__ldg(qp), __ldg(qp + 1), __ldg(qp + 2), __ldg(qp + 3)};
+    const double ls[3] = {__ldg(lsp), __ldg(lsp + 1), __ldg(lsp + 2)};
     double qn = __dsqrt_rn(add(add(add(mul(q[0], q[0]), mul(q[1], q[1])), mul(q[2], q[2])),
                                mul(q[3], q[3])));
     double qw = q[0] / qn, qx = q[1] / qn, qy = q[2] / qn, qz = q[3] / qn;
@@ -161,7 +168,6 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     R[2][0] = 2.0 * sub(mul(qx, qz), mul(qw, qy));
     R[2][1] = 2.0 * add(mul(qy, qz), mul(qw, qx));
     R[2][2] = 1.0 - 2.0 * add(mul(qx, qx), mul(qy, qy));
-    const double* ls = A.cloud.log_scales + 3 * i;
     double s0 = exp(ls[0]), s1 = exp(ls[1]), s2 = exp(ls[2]);
     double M[3][3];
 #pragma unroll
@@ -192,9 +198,8 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
                       mul(WS[r][2], W[3 * c + 2]));
     // the MLP's elevation input (mlp.py:88, unclamped) from the view-space
     // position, recomputed here with the view chain's operations
-    const double* P = A.cloud.positions + 3 * i;
-    const double p0 = sub(P[0], A.pose.rx[0]), p1 = sub(P[1], A.pose.rx[1]),
-                 p2 = sub(P[2], A.pose.rx[2]);
+    const double p0 = sub(P0, A.pose.rx[0]), p1 = sub(P1, A.pose.rx[1]),
+                 p2 = sub(P2, A.pose.rx[2]);
     const double vx = dot3_seq(p0, p1, p2, W[0], W[1], W[2]);
     const double vy = dot3_seq(p0, p1, p2, W[3], W[4], W[5]);
     const double vz = dot3_seq(p0, p1, p2, W[6], W[7], W[8]);
