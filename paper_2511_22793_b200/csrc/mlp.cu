@@ -18,6 +18,8 @@
 
 namespace gs {
 
+long long* dbg_rows(int which);
+
 struct MlpArgs {
   const float* w32;
   const double* w64;
@@ -31,6 +33,7 @@ struct MlpArgs {
   void* coef;
   int64_t n;
   int stream_ctas;  // > 0: started during pass A (PDL); entries appear as its CTAs finish
+  long long* dbg;   // experiments: per-CTA start/end stamps (GSPARC_MLP_DBG)
   int B, C, H, I, P;
   int64_t Cp;  // B*C
 };
@@ -167,6 +170,10 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
+  // streaming (render path): pass B may run its prologue (it waits for this
+  // grid).  Not otherwise: a pass A launched next would read coef early.
+  if (A.stream_ctas) pdl_trigger();
   if (A.live_list && A.stream_ctas) {
     // streaming: the list is -1 where pass A has not written yet (K2 clears
     // it); a warp takes entries wid, wid + nwarps, ... as they appear, and
@@ -186,6 +193,11 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
       }
       if (v < 0) break;
       mlp_wide_one(A, v, lane);
+      if (A.dbg && lane == 0) atomicMax(A.dbg + blockIdx.x * 16 + 13, (long long)gtimer());
+    }
+    if (A.dbg) {
+      __syncthreads();
+      if (threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 15] = gtimer();
     }
     pdl_wait();  // complete only after pass A has
     return;
@@ -209,6 +221,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
                const gsparc_frame_layout& L, char* frame, cudaStream_t st, int stream_ctas) {
   MlpArgs A;
   A.stream_ctas = 0;
+  A.dbg = getenv("GSPARC_MLP_DBG") ? dbg_rows(3) + 16 * 2048 : nullptr;  // experiments only
   A.w32 = cloud.mlp_weights;
   A.w64 = cloud.mlp_weights64;
   A.pos = cloud.positions;

@@ -3,7 +3,7 @@ start/end stamps of K3 (per tile), K4a and K4b (per half-tile CTA) from the
 same render, list lengths and pass A's chunks with contributions."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-for e in ("GSPARC_SORT_DBG", "GSPARC_PXA_DBG", "GSPARC_PXB_DBG"):
+for e in ("GSPARC_SORT_DBG", "GSPARC_PXA_DBG", "GSPARC_PXB_DBG", "GSPARC_MLP_DBG"):
     os.environ[e] = "1"
 import numpy as np, torch
 import bench
@@ -17,9 +17,9 @@ L = _lib.lib()
 for _ in range(5):
     img, frame = R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=True)
 torch.cuda.synchronize()
-host = (ctypes.c_longlong * (12288 * 16))()
-assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
-D = np.ctypeslib.as_array(host).reshape(3, 4096, 16)
+host = (ctypes.c_longlong * (16384 * 16))()
+assert L.gsparc_debug_copy(host, ctypes.c_int64(16384 * 16)) == 0
+D = np.ctypeslib.as_array(host).reshape(4, 4096, 16)
 nt = 138
 ds, da, db = D[0, :nt], D[1, :2 * nt], D[2, :2 * nt]
 ts = frame.view("tile_start", torch.int32, (nt + 1,)).cpu().numpy()
@@ -32,6 +32,9 @@ b0, b1 = us(db[:, 12]), us(db[:, 15])
 print("times in us from the first K3 CTA start")
 print("K3  start %.1f..%.1f end max %.1f mean %.1f" % (s0.min(), s0.max(), s1.max(), s1.mean()))
 print("K4a start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (a0.min(), a0.max(), a1.max(), (a1 - a0).max(), (a1 - a0).mean()))
+dm = D[3, 2048:2048 + 148]
+m0, m1, mw = us(dm[:, 14]), us(dm[:, 15]), us(dm[:, 13])
+print("K1  start %.1f..%.1f last Gaussian done %.1f end max %.1f" % (m0.min(), m0.max(), mw[dm[:, 13] > 0].max(), m1.max()))
 print("K4b start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (b0.min(), b0.max(), b1.max(), (b1 - b0).max(), (b1 - b0).mean()))
 wait = a0 - np.repeat(s1, 2)
 print("pass A start - own sort end: min %.1f max %.1f mean %.1f" % (wait.min(), wait.max(), wait.mean()))
