@@ -33,6 +33,9 @@ struct PrepArgs {
   int64_t capacity;
   int seg_stride;
   long long* dbg;  // experiments: per-CTA phase clocks (GSPARC_PREP_DBG)
+  int bin_small;   // rectangles up to this many tiles are binned by one thread
+                   // (40: K2 24.5 -> 22.6 us on config 3; 8 was slower than
+                   // none -- the average rectangle has ~10 tiles)
 };
 
 __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, double b0, double b1,
@@ -41,6 +44,33 @@ __device__ __forceinline__ double dot3_seq(double a0, double a1, double a2, doub
 }
 
 __device__ __forceinline__ double np_floor_div16(double v) { return floor(v / 16.0); }
+
+
+// Visits every (tile, Gaussian) pair of the warp's Gaussians flagged in bigm,
+// one Gaussian at a time, consecutive tiles of its rectangle (row-major, the
+// seam-wrapped range after the main one) on consecutive lanes.  Warp-uniform.
+template <typename F>
+__device__ __forceinline__ void for_big_tiles(unsigned bigm, int ry0, int ry1, int ra0, int ra1,
+                                              int rb0, int rb1, uint64_t payload, int lane,
+                                              int ntx, F f) {
+  while (bigm) {
+    const int src = __ffs(bigm) - 1;
+    bigm &= bigm - 1;
+    const int y0 = __shfl_sync(0xffffffffu, ry0, src), y1 = __shfl_sync(0xffffffffu, ry1, src);
+    const int a0 = __shfl_sync(0xffffffffu, ra0, src), a1 = __shfl_sync(0xffffffffu, ra1, src);
+    const int b0 = __shfl_sync(0xffffffffu, rb0, src), b1 = __shfl_sync(0xffffffffu, rb1, src);
+    const uint64_t v =
+        ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(payload >> 32), src) << 32) |
+        __shfl_sync(0xffffffffu, (uint32_t)payload, src);
+    const int na = a1 - a0 + 1, nb = b1 >= b0 ? b1 - b0 + 1 : 0, nrow = na + nb;
+    const int total = (y1 - y0 + 1) * nrow;
+    for (int j = lane; j < total; j += 32) {
+      const int r = j / nrow, cc = j - r * nrow;
+      const int tx = cc < na ? a0 + cc : b0 + (cc - na);
+      f((y0 + r) * ntx + tx, v);
+    }
+  }
+}
 
 // Tile binning is fused in (the counting-sort digit of rasterizer.py:115-145's
 // per-tile lists): every CTA histograms its Gaussians' tile rectangles,
@@ -75,6 +105,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   const bool valid = i < A.cloud.n;
   const double* W = A.pose.W;
   bool kept_out = false;
+  int np_out = 0;
   uint64_t packed = 0;
   int ry0 = 0, ry1 = -1, ra0 = 0, ra1 = -1, rb0 = 0, rb1 = -1;
   double x = 0, y = 0, z = 0, depth = 0, theta = 0, mx = 0, my = 0, rho2_u = 0;
@@ -312,13 +343,14 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     A.live_list[i] = -1;  // entries appear as pass A appends them (streaming K1)
     A.rect[i] = make_int4(y0 | (y1 << 16), (a0 & 0xffff) | (a1 << 16), (b0 & 0xffff) | (b1 << 16),
                           npairs);
-    if (keep) {
+    if (keep && npairs <= A.bin_small) {  // larger rectangles: whole warp, below
       for (int ty = y0; ty <= y1; ++ty) {
         for (int tx = a0; tx <= a1; ++tx) atomicAdd(s_tiles + ty * ntx + tx, 1);
         for (int tx = b0; tx <= b1; ++tx) atomicAdd(s_tiles + ty * ntx + tx, 1);
       }
     }
     kept_out = keep;
+    np_out = npairs;
     packed = ((uint64_t)(uint32_t)((k - DEPTH_KEY_BASE) >> COARSE_SHIFT) << 32) | (uint32_t)i;
     ry0 = y0;
     ry1 = y1;
@@ -331,6 +363,12 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     unsigned kept_warp = __reduce_add_sync(0xffffffffu, kept_out ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
   }
+  // rectangles of more than bin_small tiles are expanded by the whole warp,
+  // one Gaussian at a time, a tile per lane (a per-thread loop would hold
+  // the warp for the largest rectangle's count of dependent atomics)
+  const unsigned bigm = __ballot_sync(0xffffffffu, kept_out && np_out > A.bin_small);
+  for_big_tiles(bigm, ry0, ry1, ra0, ra1, rb0, rb1, packed, lane, A.gc.ntx,
+                [&](int t, uint64_t) { atomicAdd(s_tiles + t, 1); });
   __syncthreads();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_d0;  // rect+hist
   block_exclusive_scan(s_tiles, s_off, ntiles, s_tmp);  // ends with a barrier
@@ -354,7 +392,10 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   }
   __syncthreads();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 11] = clock64() - t_d0;
-  if (kept_out && fits) {
+  if (fits)
+    for_big_tiles(bigm, ry0, ry1, ra0, ra1, rb0, rb1, packed, lane, A.gc.ntx,
+                  [&](int t, uint64_t v) { A.stage[atomicAdd(s_off + t, 1)] = v; });
+  if (kept_out && fits && np_out <= A.bin_small) {
     const int ntx = A.gc.ntx;
     for (int ty = ry0; ty <= ry1; ++ty) {
       for (int tx = ra0; tx <= ra1; ++tx) {
@@ -398,6 +439,7 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.capacity = L.pair_capacity;
   A.seg_stride = (int)L.seg_stride;
   A.dbg = getenv("GSPARC_PREP_DBG") ? dbg_rows(3) : nullptr;  // experiments only
+  A.bin_small = getenv("GSPARC_BIN_SMALL") ? atoi(getenv("GSPARC_BIN_SMALL")) : 40;
   // counters | tile_count | tile_cursor are laid out back to back
   const int64_t zero_end = L.off_tile_cursor + (int64_t)sizeof(int) * L.ntiles;
   if (L.off_tile_count < L.off_counters || L.off_tile_cursor < L.off_tile_count) {
