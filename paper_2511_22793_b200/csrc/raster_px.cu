@@ -61,6 +61,7 @@ struct PxArgs {
   float4* pxw;    // [2*ntiles][wmax][8][128] weights of the first wmax chunks
   uint32_t* ch_wm;  // [slots][4] per-warp included-entry mask
   const int* ready;  // pass A: K3's per-tile flags (null: the sort grid has completed)
+  int pdl_b;         // pass B launched as a dependent (upstream reads after the wait)
   int wmax;
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
@@ -538,6 +539,15 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CtaGeom g = cta_geom(A, blockIdx.x);
   const int col0 = blockIdx.y * NP;
+  // ordinary launch: the chunk count and list bounds are read first so their
+  // latency overlaps the prologue; a dependent launch reads them after its
+  // grid-dependency wait
+  int64_t slot0 = 0;
+  int nch = 0;
+  if (!A.pdl_b) {
+    slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
+    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[blockIdx.x] : 0;
+  }
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
@@ -566,10 +576,15 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   // launched as a dependent of the previous kernel (the lazy MLP or pass A):
   // the prologue above overlaps its tail; nothing upstream is read before
   // this wait
-  pdl_wait();
-  const int64_t slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
-  const int nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[blockIdx.x] : 0;
-  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
+  if (A.pdl_b) {
+    pdl_wait();
+    slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
+    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[blockIdx.x] : 0;
+  }
+  if (A.dbg && threadIdx.x == 0) {
+    A.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
+    A.dbg[blockIdx.x * 16 + 5] = gtimer();  // upstream grid complete
+  }
 
   if (warp < 8) {
     // ---------------- weight groups: group gq takes chunks c = gq (mod 2)
@@ -894,13 +909,16 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   }
   PxArgs B = A;
   B.dbg = nullptr;
+  B.pdl_b = 0;
   if (getenv("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   // dependent launch behind the streaming MLP (render path, pass 2): the
   // prologue (TMEM allocation, barriers, stage clearing) overlaps the MLP's
   // tail.  Measured: config 5 +4.7%, config 3 neutral; directly behind pass
   // A (pass 0) the early CTAs only park on the SMs (config 1 -2.5%).
   static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_B");
-  const bool pdl = pdl_env && after_mlp;
+  // (one channel chunk, e.g. config 3: an ordinary launch with the reads
+  // ahead of the prologue is as fast)
+  const bool pdl = pdl_env && after_mlp && chunks_y > 1;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(A.ntiles * 2, chunks_y);
@@ -912,6 +930,7 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    B.pdl_b = 1;
   }
   cudaLaunchKernelEx(&cfg, k_pxb<NP>, B);
 }
@@ -941,6 +960,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.ch_wm = (uint32_t*)(frame + L.off_ch_wm);
   A.wmax = (int)L.pxw_chunks;
   A.ready = nullptr;
+  A.pdl_b = 0;
   A.Cp = (int64_t)n_tx * C;
   A.n = L.n;
   A.C = C;

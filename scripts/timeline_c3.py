@@ -35,6 +35,10 @@ print("K4a start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (a0.min(), a
 dm = D[3, 2048:2048 + 148]
 m0, m1, mw = us(dm[:, 14]), us(dm[:, 15]), us(dm[:, 13])
 print("K1  start %.1f..%.1f last Gaussian done %.1f end max %.1f" % (m0.min(), m0.max(), mw[dm[:, 13] > 0].max(), m1.max()))
+bw = us(db[:, 5])
+print("K4b work start (after the grid-dependency wait) %.1f..%.1f; work dur max %.1f mean %.1f" % (bw.min(), bw.max(), (b1 - bw).max(), (b1 - bw).mean()))
+for c in np.argsort(-(b1 - bw))[:6]:
+    print("  K4b cta", c, "nch", db[c, 11], "placed %.1f work %.1f..%.1f" % (b0[c], bw[c], b1[c]))
 print("K4b start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (b0.min(), b0.max(), b1.max(), (b1 - b0).max(), (b1 - b0).mean()))
 wait = a0 - np.repeat(s1, 2)
 print("pass A start - own sort end: min %.1f max %.1f mean %.1f" % (wait.min(), wait.max(), wait.mean()))
