@@ -62,6 +62,7 @@ struct PxArgs {
   uint32_t* ch_wm;  // [slots][4] per-warp included-entry mask
   const int* ready;  // pass A: K3's per-tile flags (null: the sort grid has completed)
   int pdl_b;         // pass B launched as a dependent (upstream reads after the wait)
+  int mix_b;         // pass B: interleave top/bottom tiles in launch order
   int wmax;
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
@@ -535,9 +536,18 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   __shared__ int s_acc;   // accumulator initialised (an MMA was issued)
 
   const long long t_start = clock64();
-  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 12] = gtimer();
+  // (tile, half) of this CTA: with mix_b, consecutive CTAs alternate between
+  // a tile of the top half of the image and one of the bottom half, so the
+  // two CTAs an SM receives together rarely are both of a heavy tile row
+  int cta = blockIdx.x;
+  if (A.mix_b) {
+    const int k = blockIdx.x >> 1, nt = A.ntiles;
+    const int tile = (k & 1) ? nt - 1 - (k >> 1) : (k >> 1);
+    cta = 2 * tile + (blockIdx.x & 1);
+  }
+  if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 12] = gtimer();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const CtaGeom g = cta_geom(A, blockIdx.x);
+  const CtaGeom g = cta_geom(A, cta);
   const int col0 = blockIdx.y * NP;
   // ordinary launch: the chunk count and list bounds are read first so their
   // latency overlaps the prologue; a dependent launch reads them after its
@@ -546,7 +556,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   int nch = 0;
   if (!A.pdl_b) {
     slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
-    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[blockIdx.x] : 0;
+    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[cta] : 0;
   }
 
   if (threadIdx.x == 0) {
@@ -579,11 +589,11 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   if (A.pdl_b) {
     pdl_wait();
     slot0 = chunk_slot0(A.tile_start, g.tile, g.half);
-    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[blockIdx.x] : 0;
+    nch = g.any && !A.counters[GSPARC_CNT_OVERFLOW] ? A.ch_n[cta] : 0;
   }
   if (A.dbg && threadIdx.x == 0) {
-    A.dbg[blockIdx.x * 16 + 13] = clock64() - t_start;
-    A.dbg[blockIdx.x * 16 + 5] = gtimer();  // upstream grid complete
+    A.dbg[cta * 16 + 13] = clock64() - t_start;
+    A.dbg[cta * 16 + 5] = gtimer();  // upstream grid complete
   }
 
   if (warp < 8) {
@@ -664,7 +674,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       float4 wr[PX_K / 4];
       if (wp) {  // this pixel's stored weights (none stored: all zero)
         const uint32_t wm = nwm;
-        const float4* src = A.pxw + ((int64_t)blockIdx.x * A.wmax + c) * 8 * 128 + q * 32 + lane;
+        const float4* src = A.pxw + ((int64_t)cta * A.wmax + c) * 8 * 128 + q * 32 + lane;
 #pragma unroll
         for (int j = 0; j < PX_K / 4; ++j)
           wr[j] = wm ? __ldcg(src + j * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -811,8 +821,8 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     if (c < nch) prefetch(c, false);
     for (; c < nch; c += 2) chunk(std::integral_constant<bool, false>(), c);
     if (A.dbg && lane == 0 && q == 0) {
-      A.dbg[blockIdx.x * 16 + 6 + gq] = tw;
-      A.dbg[blockIdx.x * 16 + 8 + gq] = tc;
+      A.dbg[cta * 16 + 6 + gq] = tw;
+      A.dbg[cta * 16 + 8 + gq] = tc;
     }
   }
 
@@ -829,7 +839,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const long long te0 = clock64();
-    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = te0 - t_start;
+    if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 14] = te0 - t_start;
     const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
 #pragma unroll 1
     for (int c0 = cbeg; c0 < cend; c0 += 8) {
@@ -874,9 +884,9 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
                  "r"(CF::TMEM_COLS));
   }
   if (A.dbg && threadIdx.x == 0) {
-    A.dbg[blockIdx.x * 16 + 10] = clock64() - t_start;
-    A.dbg[blockIdx.x * 16 + 11] = nch;
-    A.dbg[blockIdx.x * 16 + 15] = gtimer();
+    A.dbg[cta * 16 + 10] = clock64() - t_start;
+    A.dbg[cta * 16 + 11] = nch;
+    A.dbg[cta * 16 + 15] = gtimer();
   }
 }
 
@@ -910,6 +920,11 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   PxArgs B = A;
   B.dbg = nullptr;
   B.pdl_b = 0;
+  // top/bottom interleave: measured on the render path with one channel
+  // chunk (config 3: 105.8 -> 104.7 us); with a dependent launch (config 5)
+  // or behind pass A (config 1) it was 1-2% slower, so it is off there
+  static const int mix = getenv("GSPARC_PXB_MIX") ? atoi(getenv("GSPARC_PXB_MIX")) : -1;
+  B.mix_b = mix >= 0 ? mix : (after_mlp && chunks_y == 1);
   if (getenv("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   // dependent launch behind the streaming MLP (render path, pass 2): the
   // prologue (TMEM allocation, barriers, stage clearing) overlaps the MLP's
@@ -918,7 +933,8 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_B");
   // (one channel chunk, e.g. config 3: an ordinary launch with the reads
   // ahead of the prologue is as fast)
-  const bool pdl = pdl_env && after_mlp && chunks_y > 1;
+  static const bool pdl1 = getenv("GSPARC_PXB_PDL1") != nullptr;  // experiments
+  const bool pdl = pdl_env && after_mlp && (chunks_y > 1 || pdl1);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(A.ntiles * 2, chunks_y);
@@ -961,6 +977,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.wmax = (int)L.pxw_chunks;
   A.ready = nullptr;
   A.pdl_b = 0;
+  A.mix_b = 0;
   A.Cp = (int64_t)n_tx * C;
   A.n = L.n;
   A.C = C;

@@ -1,9 +1,10 @@
 """Per-CTA timeline of one config-3 render (experiments): globaltimer
-start/end stamps of K3 (per tile), K4a and K4b (per half-tile CTA) from the
-same render, list lengths and pass A's chunks with contributions."""
+start/end stamps of K2, K3 (per tile), K4a, K1 and K4b from the same render
+(replayed from a CUDA graph with the L2 flushed, as bench.py; --eager for
+host-enqueued launches), list lengths and pass A's chunks with contributions."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-for e in ("GSPARC_SORT_DBG", "GSPARC_PXA_DBG", "GSPARC_PXB_DBG", "GSPARC_MLP_DBG"):
+for e in ("GSPARC_SORT_DBG", "GSPARC_PXA_DBG", "GSPARC_PXB_DBG", "GSPARC_MLP_DBG", "GSPARC_PREP_DBG"):
     os.environ[e] = "1"
 import numpy as np, torch
 import bench
@@ -14,8 +15,28 @@ dc = DeviceCloud.from_host(cloud)
 R = Renderer()
 tx = torch.as_tensor(bench.sample_tx(1000, 1), device="cuda")
 L = _lib.lib()
-for _ in range(5):
-    img, frame = R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=True)
+img, frame = R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, lazy=True)
+torch.cuda.synchronize()
+eager = "--eager" in sys.argv
+def step():
+    R.forward(dc, ViewPose(np.zeros(3)), tx, 360, 90, frame=frame, image=img, lazy=True,
+              sync_check=False)
+if eager:  # host-enqueued launches: later kernels may wait for the host
+    for _ in range(5):
+        step()
+else:  # as bench.py: one CUDA graph per render, L2 flushed before it
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(5):
+        flush.fill_(1)
+        g.replay()
 torch.cuda.synchronize()
 host = (ctypes.c_longlong * (16384 * 16))()
 assert L.gsparc_debug_copy(host, ctypes.c_int64(16384 * 16)) == 0
@@ -24,12 +45,14 @@ nt = 138
 ds, da, db = D[0, :nt], D[1, :2 * nt], D[2, :2 * nt]
 ts = frame.view("tile_start", torch.int32, (nt + 1,)).cpu().numpy()
 ln = np.diff(ts)
-t0 = ds[:, 14].min()
+dk = D[3, :391]
+t0 = dk[:, 14].min() if dk[:, 14].max() > 0 else ds[:, 14].min()
 us = lambda v: (v - t0) / 1e3
 s0, s1 = us(ds[:, 14]), us(ds[:, 15])
 a0, a1 = us(da[:, 14]), us(da[:, 15])
 b0, b1 = us(db[:, 12]), us(db[:, 15])
-print("times in us from the first K3 CTA start")
+print("times in us from the first K2 CTA start (%s)" % ("eager" if eager else "graph, L2 flushed"))
+print("K2  start %.1f..%.1f end max %.1f" % (us(dk[:, 14]).min(), us(dk[:, 14]).max(), us(dk[:, 15]).max()))
 print("K3  start %.1f..%.1f end max %.1f mean %.1f" % (s0.min(), s0.max(), s1.max(), s1.mean()))
 print("K4a start %.1f..%.1f end max %.1f; dur max %.1f mean %.1f" % (a0.min(), a0.max(), a1.max(), (a1 - a0).max(), (a1 - a0).mean()))
 dm = D[3, 2048:2048 + 148]
