@@ -291,6 +291,9 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   const long long t_dbg0 = clock64();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
   pdl_trigger();  // pass A may be scheduled now; it waits on A.ready per tile
+  // launched as a dependent of K2: every histogram and segment is written
+  // once K2's grid has completed
+  pdl_wait();
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
   __shared__ int s_start[2];
   __shared__ int s_pos;
@@ -536,7 +539,20 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
     attr_set = smem_sort;
   }
-  k_tile_sort<<<L.ntiles, RS_T, smem_sort, st>>>(A);
+  static const bool pdl = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K3");
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(L.ntiles);
+  cfg.blockDim = dim3(RS_T);
+  cfg.dynamicSmemBytes = smem_sort;
+  cfg.stream = st;
+  if (pdl) {  // K2 triggers at its start; this launch then waits for it on the device
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  cudaLaunchKernelEx(&cfg, k_tile_sort, A);
   return check_launch("k_tile_sort");
 }
 

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   __shared__ int s_base;
   const long long t_d0 = clock64();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
+  pdl_trigger();  // K3 may be scheduled as SMs free up (it waits for this grid)
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_tiles[t] = 0;
   __syncthreads();
 
