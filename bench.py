@@ -442,8 +442,8 @@ def run_ours(args):
 
 
 def kernels_per_step(lazy):
-    # static fallback: preprocess, tile_sort, raster pass(es), mlp
-    return 5 if lazy else 4
+    # static fallback: frame clear, preprocess, tile_sort, raster pass(es), mlp
+    return 6 if lazy else 5
 
 
 def count_our_kernels(fn):

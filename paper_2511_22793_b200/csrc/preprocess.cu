@@ -360,6 +360,9 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
     rb0 = b0;
     rb1 = b1;
   }
+  // launched as a dependent of the frame-clearing kernel: the f64 chains
+  // above overlap it; the first global counter update comes after this
+  pdl_wait();
   {
     unsigned kept_warp = __reduce_add_sync(0xffffffffu, kept_out ? 1u : 0u);
     if ((threadIdx.x & 31) == 0 && kept_warp) atomicAdd(A.counters + GSPARC_CNT_KEPT, (int)kept_warp);
@@ -418,6 +421,13 @@ __global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
   }
 }
 
+// Clears the frame's counters | tile_count | tile_cursor (back to back) and
+// lets K2 start at once (K2 waits for it before its first counter update).
+__global__ void __launch_bounds__(256) k_clear_frame(int* p, int n) {
+  pdl_trigger();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
 int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
                       const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
   PrepArgs A;
@@ -447,8 +457,15 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
     set_error("preprocess: unexpected frame layout");
     return GSPARC_ERR_ARG;
   }
-  if (cudaMemsetAsync(frame + L.off_counters, 0, zero_end - L.off_counters, st) != cudaSuccess)
+  static const bool pdl = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K2");
+  if (pdl) {
+    const int nz = (int)((zero_end - L.off_counters) / (int64_t)sizeof(int));
+    k_clear_frame<<<1, 256, 0, st>>>((int*)(frame + L.off_counters), nz);
+    GS_TRY(check_launch("k_clear_frame"));
+  } else if (cudaMemsetAsync(frame + L.off_counters, 0, zero_end - L.off_counters, st) !=
+             cudaSuccess) {
     return check_launch("preprocess memset");
+  }
   if (cloud.n > 0) {
     const int blocks = (int)((cloud.n + PREP_G - 1) / PREP_G);
     if (blocks > L.seg_stride) {
@@ -456,7 +473,19 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
       return GSPARC_ERR_ARG;
     }
     const size_t smem = sizeof(int) * (2 * (size_t)L.ntiles + 1 + PREP_T / 32 + 1);
-    k_preprocess<<<blocks, PREP_T, smem, st>>>(A);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(PREP_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    if (pdl) {
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, k_preprocess, A);
   }
   return check_launch("k_preprocess");
 }

@@ -61,7 +61,7 @@ def test_plan_frame_layout(L):
     assert lay.off_stage % 256 == 0 and lay.off_seg % 256 == 0
     assert lay.off_stage + 8 * 200000 <= lay.off_seg
     assert lay.off_seg + 8 * 138 * lay.seg_stride <= lay.total_bytes
-    # counters, tile_count, tile_cursor are contiguous (one memset)
+    # counters, tile_count, tile_cursor are contiguous (one clearing kernel)
     assert lay.off_counters < lay.off_tile_count < lay.off_tile_cursor < lay.off_key
 
 
