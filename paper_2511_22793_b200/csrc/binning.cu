@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 15] = gtimer();
 }
 
-int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st) {
+int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st, bool dependent) {
   SortArgs A;
   A.pairs = (uint64_t*)(frame + L.off_pairs);
   A.tile_start = (int*)(frame + L.off_tile_start);
@@ -539,7 +539,11 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st)
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);
     attr_set = smem_sort;
   }
-  static const bool pdl = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K3");
+  // dependent launch behind K2 on the lazy render path (config 3: -0.5 us);
+  // ahead of the full MLP (config 1) it measured 5 us slower, so there the
+  // sort is an ordinary launch (griddepcontrol.wait then returns at once)
+  static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K3");
+  const bool pdl = pdl_env && dependent;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(L.ntiles);

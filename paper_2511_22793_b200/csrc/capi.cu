@@ -249,8 +249,8 @@ int gsparc_render_forward(const gsparc_cloud* cloud, const gsparc_view* view,
   cudaStream_t st = (cudaStream_t)stream;
   char* f = (char*)frame;
   GS_TRY(gsparc_prepare(cloud, view, frame, L, stream));
-  GS_TRY(launch_bin_tiles(*L, f, st));
   const bool lazy = (flags & GSPARC_LAZY_MLP) && !(flags & GSPARC_FORCE_FUSED);
+  GS_TRY(launch_bin_tiles(*L, f, st, lazy));
   if (lazy) {
     GS_TRY(launch_raster_forward(*L, f, n_tx, cloud->mlp_out, t_eps, 1, image_out, st));
     // f32 frames: the MLP streams the live list while pass A finishes

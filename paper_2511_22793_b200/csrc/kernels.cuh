@@ -9,7 +9,8 @@ int forward_sub_rows(const gsparc_frame_layout& L, int64_t Cp);
 
 int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
                       const gsparc_frame_layout& L, char* frame, cudaStream_t st);
-int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st);
+int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st,
+                     bool dependent = false);
 int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_only,
                const gsparc_frame_layout& L, char* frame, cudaStream_t st, int stream_ctas = 0);
 int launch_raster_forward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
