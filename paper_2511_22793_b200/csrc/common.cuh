@@ -230,6 +230,19 @@ __device__ __forceinline__ FastAlpha fast_alpha_full(float pcx, float pcy, float
   return o;
 }
 
+// alpha before the 1/255 cut: min(2^(q' + log2 sigma), 0.99); the cut
+// (alpha = 0 below ALPHA_MIN_F) is raw >= ALPHA_MIN_F, the same test as
+// fast_alpha's a > 0 (ALPHA_MAX_F > ALPHA_MIN_F), folded into the caller's
+// predicate
+__device__ __forceinline__ float fast_alpha_uncut(float pcx, float pcy, float4 r0, float4 r1,
+                                                  float w, float inv_w) {
+  const float dxr = pcx - r0.x;
+  const float dx = fmaf(-w, rintf(dxr * inv_w), dxr);
+  const float dy = pcy - r0.y;
+  const float t = fmaf(r0.w, dy, r0.z * dx);
+  return fminf(ex2_approx(fmaf(dx, t, fmaf(r1.x * dy, dy, r1.y))), ALPHA_MAX_F);
+}
+
 __device__ __forceinline__ float fast_alpha(float pcx, float pcy, float4 r0, float4 r1, float w,
                                             float inv_w) {
   const float dxr = pcx - r0.x;

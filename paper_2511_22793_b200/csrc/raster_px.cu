@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
 #pragma unroll
         for (int k = 0; k < PX_K; ++k) {
           const float4 r0 = s_ring[s][k][0], r1 = s_ring[s][k][1];
-          const float a = fast_alpha(pcx, pcy, r0, r1, wf, inv_w);
-          const bool act = Tl >= teps && a > 0.f;
+          const float a = fast_alpha_uncut(pcx, pcy, r0, r1, wf, inv_w);
+          const bool act = Tl >= teps && a >= ALPHA_MIN_F;  // = fast_alpha(..) > 0
           const float wgt = act ? Tl * a : 0.f;
           if (SC) {
             const float4 cf = *(const float4*)&s_cf[s][k][0];
