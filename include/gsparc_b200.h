@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define GSPARC_ABI_VERSION 3
+#define GSPARC_ABI_VERSION 4
 
 enum {
   GSPARC_OK = 0,
@@ -230,7 +230,10 @@ int64_t gsparc_loss_scratch_bytes(int32_t n_img, int32_t height, int32_t width,
  * sigma 1.5, reflect padding); dimg = dloss/dimg chained through the
  * magnitude.  img/gt/dimg in `dtype` (GSPARC_F32 / GSPARC_F64); gt has
  * 1 (magnitude) or C channels; arithmetic is f64.
- * stats_out: f64 [n_img, 4] = (loss, l1, ssim, mse) per image. */
+ * stats_out: f64 [n_img, GSPARC_LOSS_STATS] = (loss, l1, ssim, mse,
+ * ssim of channel 0, mse of channel 0) per image; the last two are what the
+ * reference's train_step logs (optimize.py:281,293). */
+#define GSPARC_LOSS_STATS 6
 int gsparc_loss_fwd_bwd(const void* img_dev, const void* gt_dev,
                         int32_t dtype, int32_t n_img, int32_t height,
                         int32_t width, int32_t channels, int32_t supervision,

@@ -12,7 +12,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsparc_b200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
+LOSS_STATS = 6  # GSPARC_LOSS_STATS
 
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
 F32, F64 = 0, 1

@@ -34,7 +34,7 @@ struct SortArgs {
   const uint64_t* stage;
   int64_t seg_stride;
   uint64_t* sort_tmp;  // [pair_capacity] scratch for lists beyond shared memory
-  int* inv;          // deterministic frames: [n][DET_MAXT] list positions
+  int* inv;          // deterministic frames: [n][ntiles] list positions
   const int4* rect;  // tile rectangles (K2)
   int ntx;
   int ntiles;
@@ -339,7 +339,16 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   }
   __syncthreads();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 1] = clock64() - t_dbg0;
-  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
+  if (A.counters[GSPARC_CNT_OVERFLOW]) {
+    // the staged pairs are incomplete: no list, but the tile is still
+    // published so that pass-A CTAs waiting on the queue see the overflow
+    // (K2 has completed, so the flag is final) and exit
+    if (threadIdx.x == 0) {
+      const int q = atomicAdd(A.counters + GSPARC_CNT_SORTED, 1);
+      flag_release(A.ready + q, t + 1);
+    }
+    return;
+  }
   const int s = s_start[0], n = s_start[1] - s;
   uint64_t* g = A.pairs + s;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
@@ -492,7 +501,9 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       const int y0 = rc.x & 0xffff, a0 = rc.y & 0xffff, a1 = rc.y >> 16, b1 = rc.z >> 16;
       const int na = a1 - a0 + 1, nbo = b1 >= 0 ? min(b1, a0 - 1) + 1 : 0;
       const int slot = (ty - y0) * (na + nbo) + (tx >= a0 && tx <= a1 ? tx - a0 : na + tx);
-      if (slot >= 0 && slot < DET_MAXT) A.inv[(int64_t)idx * DET_MAXT + slot] = s + j;
+      // slot < rows * (na + nbo) <= nty * ntx: the table has ntiles slots
+      // per Gaussian (capi.cu gsparc_plan_frame), so no slot is dropped
+      A.inv[(int64_t)idx * A.ntiles + slot] = s + j;
     }
   }
   // publish the tile: its bounds (same values CTA 0 wrote) and list, then

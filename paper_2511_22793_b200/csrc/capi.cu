@@ -184,7 +184,9 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   }
   L.off_pxw = take(4 * 2 * (int64_t)L.ntiles * L.pxw_chunks * 128 * 32);
   L.off_ch_wm = take(dtype == GSPARC_F32 ? 4 * 4 * L.ch_slots : 0);
-  L.off_det_inv = det ? take(sizeof(int) * nn * DET_MAXT) : 0;
+  // a Gaussian's rectangle covers at most nty rows x ntx columns (the wrap
+  // segment never adds columns beyond ntx), so ntiles slots always suffice
+  L.off_det_inv = det ? take(sizeof(int) * nn * (int64_t)L.ntiles) : 0;
   L.off_sort_tmp = take(8 * pair_capacity);
   L.total_bytes = o;
   *out = L;

@@ -36,7 +36,7 @@ struct LossArgsT {
   double* XY;    // [2][NI][S][h][w] prediction and ground truth (f64)
   double* sums;  // [NI * S][LOSS_RB][3] per-plane partial (ssim, l1, sq) sums
   double* V3;    // [3][tot] per-pixel (ssim, l1, sq) terms
-  double* stats; // [NI][4]
+  double* stats; // [NI][GSPARC_LOSS_STATS]
   int NI, S, C, h, w, sup;
   double lam;
 };
@@ -240,7 +240,7 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
   if (b >= A.NI) return;
   const double* sm = A.sums + (int64_t)b * A.S * LOSS_RB * 3;
   const double n = (double)A.h * A.w;
-  double ss = 0.0, l1s = 0.0, sqs = 0.0;
+  double ss = 0.0, l1s = 0.0, sqs = 0.0, ss0 = 0.0, sq0 = 0.0;
   for (int s = 0; s < A.S; ++s) {
     double t[3] = {0.0, 0.0, 0.0};
     for (int rb = 0; rb < LOSS_RB; ++rb)
@@ -248,13 +248,22 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
     ss += t[0] / n;
     l1s += t[1];
     sqs += t[2];
+    if (s == 0) {
+      ss0 = t[0] / n;
+      sq0 = t[2] / n;
+    }
   }
   ss /= A.S;
   const double l1 = l1s / (n * A.S);
-  A.stats[4 * b + 0] = (1.0 - A.lam) * l1 + A.lam * (1.0 - ss);
-  A.stats[4 * b + 1] = l1;
-  A.stats[4 * b + 2] = ss;
-  A.stats[4 * b + 3] = sqs / (n * A.S);
+  double* o = A.stats + (int64_t)GSPARC_LOSS_STATS * b;
+  o[0] = (1.0 - A.lam) * l1 + A.lam * (1.0 - ss);
+  o[1] = l1;
+  o[2] = ss;
+  o[3] = sqs / (n * A.S);
+  // channel 0 only: the reference's train_step logs ssim/psnr of
+  // pred[:,:,0] vs gt[:,:,0] (optimize.py:281,293)
+  o[4] = ss0;
+  o[5] = sq0;
 }
 
 int64_t loss_scratch_bytes(int NI, int h, int w, int C) {

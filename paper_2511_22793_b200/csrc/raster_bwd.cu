@@ -365,16 +365,15 @@ struct RedArgs {
   void* gcoef;
   void* ggeo;
   int64_t n, Cp;
-  int nchunks, ntx, nsub;
-  const int* inv;  // [n][DET_MAXT] list positions per tile slot (K3)
+  int nchunks, ntx, nsub, ntiles;
+  const int* inv;  // [n][ntiles] list positions per tile slot (K3)
 };
 
-constexpr int RED_MAXT = DET_MAXT;  // tiles per Gaussian (2 x 138 at 90x360 + seam)
+constexpr int RED_MAXT = DET_MAXT;  // tile slots staged in shared memory per pass
 
 template <typename R>
 __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
   __shared__ int s_pos[8][RED_MAXT];   // list position per enumerated tile
-  __shared__ short s_tile[8][RED_MAXT];
   __shared__ unsigned char s_vis[8][RED_MAXT];  // bit 4 copy + sub-tile: partial visited
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * 8 + warp;
@@ -382,7 +381,7 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
   R* gc = (R*)A.gcoef + i * A.Cp;
   R* gg = (R*)A.ggeo + i * 8;
   const uint64_t ki = A.key[i];
-  int ntile = 0, na = 0, nbo = 0, rows = 0, y0 = 0, a0 = 0, b1 = -1;
+  int ntile = 0, na = 0, nbo = 0, y0 = 0, a0 = 0, b1 = -1;
   if (ki != ~0ULL) {
     const int4 r = A.rect[i];
     y0 = r.x & 0xffff;
@@ -392,69 +391,74 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     b1 = r.z >> 16;  // b segment is [0, b1] (wrapped), empty if b1 < 0
     na = a1 - a0 + 1;
     nbo = b1 >= 0 ? min(b1, a0 - 1) + 1 : 0;  // b tiles outside the a range
-    rows = y1 - y0 + 1;
-    ntile = rows * (na + nbo);
+    ntile = (y1 - y0 + 1) * (na + nbo);       // <= ntiles (K3's table stride)
   }
-  if (ntile > RED_MAXT) ntile = RED_MAXT;  // cannot happen for w <= 4096
-  for (int j = lane; j < ntile; j += 32) {
-    const int ty = y0 + j / (na + nbo), rj = j % (na + nbo);
-    const int tx = rj < na ? a0 + rj : rj - na;
-    const int t = ty * A.ntx + tx;
-    // list position of (Gaussian i, tile t): recorded by K3 when it placed
-    // the entry (the first copy of a seam duplicate)
-    const int lo = __ldg(A.inv + i * DET_MAXT + j);
-    const bool twice = rj < na && b1 >= 0 && tx <= b1;  // seam duplicate
-    s_pos[warp][j] = lo;
-    s_tile[warp][j] = (short)t;
-    // which (copy, sub-tile) partials exist: K5 wrote those inside each
-    // sub-tile's visited prefix (wstop, per 32-pixel warp)
-    const int ts = A.tile_start[t];
-    unsigned vis = 0;
-    for (int copy = 0; copy <= (twice ? 1 : 0); ++copy)
-      for (int p = 0; p < A.nsub; ++p) {
-        const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
-        if (lo + copy - ts < nv) vis |= 1u << (4 * copy + p);
-      }
-    s_vis[warp][j] = (unsigned char)vis;
-  }
-  __syncwarp();
-  // sums in the fixed order (tile slot, copy, sub-tile[, chunk]); the (up to
-  // 8) partials of a slot are loaded together
   const R* dgc = (const R*)A.dgc;
   const R* dgg = (const R*)A.dgg;
-  for (int64_t c0 = 0; c0 < A.Cp; c0 += 32) {
-    const int64_t cc = c0 + lane;
-    R acc = R(0);
-    if (cc < A.Cp) {
-      for (int j = 0; j < ntile; ++j) {
-        const int64_t k0 = s_pos[warp][j];
-        const unsigned vis = s_vis[warp][j];
-        R v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          v[q] = ((vis >> q) & 1u)
-                     ? dgc[((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.Cp + cc]
-                     : R(0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if ((vis >> q) & 1u) acc += v[q];
-      }
-      gc[cc] = acc;
+  // slots are taken RED_MAXT at a time (a rectangle can span every tile of
+  // a wide frame); each pass adds its fixed-order sum to the running one,
+  // so the summation order is canonical for a given frame
+  for (int j0 = 0; j0 == 0 || j0 < ntile; j0 += RED_MAXT) {
+    const int nj = min(ntile - j0, RED_MAXT);
+    __syncwarp();
+    for (int jj = lane; jj < nj; jj += 32) {
+      const int j = j0 + jj;
+      const int ty = y0 + j / (na + nbo), rj = j % (na + nbo);
+      const int tx = rj < na ? a0 + rj : rj - na;
+      const int t = ty * A.ntx + tx;
+      // list position of (Gaussian i, tile t): recorded by K3 when it placed
+      // the entry (the first copy of a seam duplicate)
+      const int lo = __ldg(A.inv + i * A.ntiles + j);
+      const bool twice = rj < na && b1 >= 0 && tx <= b1;  // seam duplicate
+      s_pos[warp][jj] = lo;
+      // which (copy, sub-tile) partials exist: K5 wrote those inside each
+      // sub-tile's visited prefix (wstop, per 32-pixel warp)
+      const int ts = A.tile_start[t];
+      unsigned vis = 0;
+      for (int copy = 0; copy <= (twice ? 1 : 0); ++copy)
+        for (int p = 0; p < A.nsub; ++p) {
+          const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
+          if (lo + copy - ts < nv) vis |= 1u << (4 * copy + p);
+        }
+      s_vis[warp][jj] = (unsigned char)vis;
     }
-  }
-  if (lane < 8) {
-    R acc = R(0);
-    if (lane < 6) {
-      for (int j = 0; j < ntile; ++j) {
-        const int64_t k0 = s_pos[warp][j];
-        const unsigned vis = s_vis[warp][j];
-        for (int q = 0; q < 8; ++q)
-          if ((vis >> q) & 1u)
-            for (int ch = 0; ch < A.nchunks; ++ch)
-              acc += dgg[(((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.nchunks + ch) * 6 + lane];
+    __syncwarp();
+    // sums in the fixed order (tile slot, copy, sub-tile[, chunk]); the (up to
+    // 8) partials of a slot are loaded together
+    for (int64_t c0 = 0; c0 < A.Cp; c0 += 32) {
+      const int64_t cc = c0 + lane;
+      if (cc < A.Cp) {
+        R acc = R(0);
+        for (int jj = 0; jj < nj; ++jj) {
+          const int64_t k0 = s_pos[warp][jj];
+          const unsigned vis = s_vis[warp][jj];
+          R v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            v[q] = ((vis >> q) & 1u)
+                       ? dgc[((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.Cp + cc]
+                       : R(0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if ((vis >> q) & 1u) acc += v[q];
+        }
+        gc[cc] = j0 == 0 ? acc : gc[cc] + acc;
       }
     }
-    gg[lane] = acc;
+    if (lane < 8) {
+      R acc = R(0);
+      if (lane < 6) {
+        for (int jj = 0; jj < nj; ++jj) {
+          const int64_t k0 = s_pos[warp][jj];
+          const unsigned vis = s_vis[warp][jj];
+          for (int q = 0; q < 8; ++q)
+            if ((vis >> q) & 1u)
+              for (int ch = 0; ch < A.nchunks; ++ch)
+                acc += dgg[(((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.nchunks + ch) * 6 + lane];
+        }
+      }
+      gg[lane] = j0 == 0 ? acc : gg[lane] + acc;
+    }
   }
 }
 
@@ -533,6 +537,7 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
   R.nchunks = A.nchunks;
   R.ntx = L.ntx;
   R.nsub = A.nsub;
+  R.ntiles = L.ntiles;
   R.inv = (const int*)(frame + L.off_det_inv);
   const unsigned blocks = (unsigned)((L.n + 7) / 8);
   if (blocks == 0) return GSPARC_OK;

@@ -155,14 +155,16 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   __shared__ __align__(8) uint64_t s_full[PX_RING], s_empty[PX_RING];
   __shared__ int s_ndone, s_nch, s_stop[4];
 
-  if (A.counters[GSPARC_CNT_OVERFLOW]) return;
   const long long t_startA = clock64();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int cta = blockIdx.x;  // (tile, half) = (cta >> 1, cta & 1)
   if (A.ready) {
     // launched while K3 runs: claim the next (tile, half) in the order the
-    // sorts finished and wait until it is published (bounded: a frame whose
-    // sort never ran reports an error instead of hanging)
+    // sorts finished and wait until it is published.  K3 publishes every
+    // tile, also on a pair-buffer overflow (then without a list), so the
+    // overflow flag is read only after the acquire, which orders it after
+    // K2's grid.  A wait that never ends (a frame whose sort did not run)
+    // is bounded: the CTA flags an error and exits without touching the tile.
     __shared__ int s_cta;
     if (threadIdx.x == 0) {
       const int h = atomicAdd(A.counters + GSPARC_CNT_CLAIMED, 1) % (2 * A.ntiles);
@@ -170,16 +172,24 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       int v;
       while (!(v = flag_acquire(A.ready + (h >> 1)))) {
         __nanosleep(64);
-        if (++spins > (1ll << 24)) {
-          atomicExch(A.counters + GSPARC_CNT_OVERFLOW, 2);
-          v = (h >> 1) + 1;
-          break;
-        }
+        if (++spins > (1ll << 24)) break;
       }
-      s_cta = 2 * (v - 1) + (h & 1);
+      if (!v) {
+        atomicExch(A.counters + GSPARC_CNT_OVERFLOW, 2);
+        s_cta = -2;
+      } else {
+        s_cta = flag_acquire(A.counters + GSPARC_CNT_OVERFLOW) ? -1 : 2 * (v - 1) + (h & 1);
+      }
     }
     __syncthreads();
     cta = s_cta;
+    if (cta == -2) return;  // the sort grid never published: do not wait on it
+    if (cta < 0) {
+      pdl_wait();
+      return;
+    }
+  } else if (A.counters[GSPARC_CNT_OVERFLOW]) {
+    return;
   }
   if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 14] = gtimer();
   pdl_trigger();  // the lazy MLP (K1) may start and consume the live list as it grows

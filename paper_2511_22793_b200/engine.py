@@ -31,6 +31,21 @@ def dtype_code(dtype):
     raise ValueError(f"unsupported render dtype {dt}")
 
 
+def view_cstruct(pose, w, h):
+    """C view for any pose object with the reference ViewPose's fields
+    (`rx_position` (3,), `rotation` (3,3); geometry.py:34-47), so
+    `rfsplat.geometry.ViewPose` works unchanged."""
+    v = _lib.CView()
+    rx = np.asarray(pose.rx_position, np.float64).reshape(3)
+    rot = np.asarray(pose.rotation, np.float64).reshape(9)
+    for k in range(3):
+        v.rx[k] = float(rx[k])
+    for k in range(9):
+        v.rotation[k] = float(rot[k])
+    v.width, v.height = int(w), int(h)
+    return v
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -163,7 +178,7 @@ class Renderer:
             lazy = C >= 16
         flags = _lib.LAZY_MLP if lazy else 0
         cc = cloud.cstruct()
-        view = pose.cstruct(w, h)
+        view = view_cstruct(pose, w, h)
         for _ in range(3):
             check(lib().gsparc_render_forward(
                 ctypes.byref(cc), ctypes.byref(view),
@@ -193,7 +208,7 @@ class Renderer:
             grad = torch.empty(n * (11 + P), dtype=_TORCH_DT[grad_dtype_code],
                                device=self.device)
         cc = cloud.cstruct()
-        view = pose.cstruct(frame.w, frame.h)
+        view = view_cstruct(pose, frame.w, frame.h)
         check(lib().gsparc_render_backward(
             ctypes.byref(cc), ctypes.byref(view),
             ctypes.c_void_p(txs.data_ptr()), int(txs.shape[0]),
@@ -221,7 +236,8 @@ class LossWorkspace:
     def __init__(self, n_img, h, w, C, device, dtype=torch.float32):
         nbytes = int(lib().gsparc_loss_scratch_bytes(n_img, h, w, C))
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        self.stats = torch.zeros((n_img, 4), dtype=torch.float64, device=device)
+        self.stats = torch.zeros((n_img, _lib.LOSS_STATS), dtype=torch.float64,
+                                 device=device)
         self.dimg = torch.empty((n_img, h, w, C), dtype=dtype, device=device)
         self.dtype_code = _lib.F64 if dtype == torch.float64 else _lib.F32
         self.shape = (n_img, h, w, C)

@@ -33,14 +33,8 @@ class ViewPose:
                              "(det +1)")
 
     def cstruct(self, w, h):
-        from ._lib import CView
-        v = CView()
-        for k in range(3):
-            v.rx[k] = float(self.rx_position[k])
-        for k, x in enumerate(self.rotation.reshape(-1)):
-            v.rotation[k] = float(x)
-        v.width, v.height = int(w), int(h)
-        return v
+        from .engine import view_cstruct
+        return view_cstruct(self, w, h)
 
 
 def pixel_to_direction(u, v, w, h):

@@ -152,6 +152,9 @@ class AdamState:
 
 
 def _run_adam(dev: DeviceCloud, grad_flat, state: AdamState, cfg, counters):
+    # K8 updates the f32 weights: an f64 copy made for the f64 verification
+    # path is stale from here on (rasterizer._device_cloud re-derives it)
+    dev.mlp_weights64 = None
     acfg = cfg.adam_cstruct()
     check(lib().gsparc_adam_step(
         ctypes.c_void_p(dev.positions.data_ptr()),
@@ -326,7 +329,10 @@ class Trainer:
 
     def step(self, global_indices=None):
         """One optimizer step on the given global batch of sample indices.
-        Returns the device stats tensor [B_local, 4] (loss, l1, ssim, mse)."""
+        Returns the device stats tensor [B_local, 6] (loss, l1, ssim, mse,
+        channel-0 ssim, channel-0 mse).  Asynchronous: a step whose pair
+        buffer overflowed is skipped by K8 (parameters, moments and the
+        device step counter untouched); `check()` reports it."""
         if global_indices is not None:
             self.set_batch(global_indices)
         if self.graph is not None:
@@ -343,8 +349,11 @@ class Trainer:
         return self.loss.stats
 
     def check(self):
-        """Synchronous health check: pair-buffer overflow (those steps were
-        skipped by K8) and non-finite gradients."""
+        """Synchronous health check of the last step: False if its pair
+        buffer overflowed (K8 skipped the update; the frame is grown and the
+        graph dropped, so the caller re-runs the same batch); raises
+        FloatingPointError on a non-finite gradient like the reference's
+        adam_step (optimize.py:241 -> rasterizer.py:63-66)."""
         c = self.frame.counters().cpu()
         if int(c[_lib.CNT_OVERFLOW]):
             need = int(c[_lib.CNT_PAIRS])
@@ -353,6 +362,27 @@ class Trainer:
             return False
         _raise_nonfinite(int(c[_lib.CNT_NONFINITE]))
         return True
+
+    def step_checked(self, global_indices, use_graph=True):
+        """step() + check(), re-running the batch after a buffer grow, so
+        every step applies exactly one update (the reference's semantics)."""
+        for _ in range(4):
+            stats = self.step(global_indices)
+            if self.check():
+                return stats
+            self.step_no -= 1
+            if use_graph:
+                self.capture()
+        raise RuntimeError("pair capacity could not be satisfied")
+
+    def load_cloud(self, cloud):
+        """Overwrite the device parameters from a host GaussianCloud (same
+        shapes), keeping the frame, workspaces and captured graph."""
+        for name in GROUPS:
+            t = getattr(self.dev, name)
+            t.copy_(torch.as_tensor(np.asarray(getattr(cloud, name)),
+                                    dtype=t.dtype))
+        self.dev.mlp_weights64 = None
 
     def sync_to_host(self, cloud: GaussianCloud):
         back = self.dev.to_host()
@@ -368,25 +398,49 @@ def _dataset_arrays(dataset, cfg):
     return txs, gt
 
 
+def _metrics_row(step, st, wall_ms):
+    """The reference's log row (optimize.py:288-295): loss and l1 over the
+    supervised channels, ssim_term and psnr from channel 0."""
+    m0 = float(st[5])
+    return {"iteration": step, "loss": float(st[0]), "l1": float(st[1]),
+            "ssim_term": 1.0 - float(st[4]),
+            "psnr": math.inf if m0 == 0.0 else 10.0 * math.log10(1.0 / m0),
+            "wall_ms": wall_ms}
+
+
 def train_step(cloud, pose, sample, state: AdamState, step, cfg: TrainConfig):
     """One render/loss/backward/Adam iteration for one sample
-    (optimize.py:273-296); returns the reference's metrics dict."""
+    (optimize.py:273-296); returns the reference's metrics dict.
+
+    The device trainer (frame, loss workspace, graph) is built on the first
+    call and kept on `state`; later calls only refresh the parameters (a
+    NumPy cloud may have been changed by the caller), the sample and the
+    step, so a train_step costs one upload, one step and one write-back."""
     t0 = time.perf_counter()
-    tr = Trainer(cloud, pose, cfg, [sample.tx_position],
-                 _dataset_arrays([sample], cfg)[1], batch_tx=1,
-                 start_step=step)
-    tr.state.m, tr.state.v = state.m, state.v
-    stats = tr.step([0])
+    gt = _dataset_arrays([sample], cfg)[1]
+    tr = getattr(state, "_trainer", None)
+    key = (id(cloud), cloud.n, tuple(cloud.mlp_dims), cfg.width, cfg.height,
+           cfg.supervision, cfg.deterministic)
+    if tr is None or state._trainer_key != key:
+        tr = Trainer(cloud, pose, cfg, [sample.tx_position], gt, batch_tx=1,
+                     start_step=step)
+        tr.state = state
+        state._trainer, state._trainer_key = tr, key
+    else:
+        tr.pose = pose
+        if not isinstance(cloud, DeviceCloud):
+            tr.load_cloud(cloud)
+        tr.tx_all.copy_(torch.as_tensor(
+            np.asarray(sample.tx_position, np.float64).reshape(1, 3)))
+        tr.gt_all.copy_(torch.as_tensor(gt))
+    tr.cfg = cfg
+    state.step_dev.fill_(int(step))
+    stats = tr.step_checked([0], use_graph=False)
     st = stats[0].cpu().numpy()
-    tr.check()
     if not isinstance(cloud, DeviceCloud):
         tr.sync_to_host(cloud)
     state.step = step + 1
-    m = float(st[3])
-    return {"iteration": step, "loss": float(st[0]), "l1": float(st[1]),
-            "ssim_term": 1.0 - float(st[2]),
-            "psnr": math.inf if m == 0.0 else 10.0 * math.log10(1.0 / m),
-            "wall_ms": (time.perf_counter() - t0) * 1e3}
+    return _metrics_row(step, st, (time.perf_counter() - t0) * 1e3)
 
 
 def sample_stream(n_samples, cfg: TrainConfig, start_step, n_steps, batch):
@@ -410,9 +464,15 @@ def sample_stream(n_samples, cfg: TrainConfig, start_step, n_steps, batch):
 
 def train(dataset, cfg: TrainConfig, cloud, pose, metrics_path=None,
           checkpoint_path=None, start_step=0, progress=None, group=None,
-          use_graph=True):
+          use_graph=True, check_every=1):
     """Training loop (optimize.py:299-351) on the device; mutates `cloud`
-    (host arrays are refreshed at checkpoints and at the end)."""
+    (host arrays are refreshed at checkpoints and at the end).
+
+    check_every=1 (default) checks every step on the host like the
+    reference, which applies each update and raises at once: an overflowed
+    step is re-run after growing the pair buffer, a non-finite gradient
+    raises FloatingPointError.  Larger values trade that for fewer host
+    syncs (a skipped step is then lost, not re-run)."""
     if not dataset:
         raise ValueError("dataset is empty")
     dims = {(s.spectrum.height, s.spectrum.width) for s in dataset}
@@ -437,16 +497,13 @@ def train(dataset, cfg: TrainConfig, cloud, pose, metrics_path=None,
         for k, batch in enumerate(sample_stream(len(dataset), cfg, start_step,
                                                 cfg.iterations, tr.B)):
             step = start_step + k
-            stats = tr.step(batch)
+            if check_every and (k % check_every == 0 or step == last):
+                stats = tr.step_checked(batch, use_graph)
+            else:
+                stats = tr.step(batch)
             if step % cfg.log_every == 0 or step == last:
-                if not tr.check() and use_graph:
-                    tr.capture()
                 st = stats.mean(dim=0).cpu().numpy()
-                m = float(st[3])
-                row = {"iteration": step, "loss": float(st[0]),
-                       "l1": float(st[1]), "ssim_term": 1.0 - float(st[2]),
-                       "psnr": math.inf if m == 0 else 10 * math.log10(1 / m),
-                       "wall_ms": (time.perf_counter() - t0) * 1e3}
+                row = _metrics_row(step, st, (time.perf_counter() - t0) * 1e3)
                 t0 = time.perf_counter()
                 log.append(row)
                 if writer:
@@ -457,7 +514,6 @@ def train(dataset, cfg: TrainConfig, cloud, pose, metrics_path=None,
             if checkpoint_path and cfg.checkpoint_every and \
                     (step + 1) % cfg.checkpoint_every == 0 and tr.rank == 0:
                 save_checkpoint(checkpoint_path, tr.dev)
-        tr.check()
         if not isinstance(cloud, DeviceCloud):
             tr.sync_to_host(cloud)
         if checkpoint_path and tr.rank == 0:

@@ -30,6 +30,15 @@ def golden_cloud(fx, prefix=""):
                  mlp_dims=tuple(int(v) for v in fx[prefix + "mlp_dims"]))
 
 
+def golden_pose(fx):
+    """(rx, W) of a fixture; cases written before poses were recorded use
+    the receiver at the origin with W = I."""
+    rx = np.asarray(fx["rx"], np.float64) if "rx" in fx else np.zeros(3)
+    W = np.asarray(fx["rotation"], np.float64) if "rotation" in fx \
+        else np.eye(3)
+    return rx, W
+
+
 def golden_dL(fx):
     h, w = int(fx["h"]), int(fx["w"])
     U = np.random.default_rng(int(fx["dL_seed"])).normal(size=(h, w, 2))

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import golden, golden_cloud
+from conftest import golden, golden_cloud, golden_pose
 
 pytestmark = pytest.mark.gpu
 
@@ -78,12 +78,21 @@ def assert_tiles_equal(aux, fx):
 
 GOLD = ["ka_single", "ka_two", "ka_clamp", "ka_near", "rand96_0", "rand96_1",
         "rand96_2", "f64_noexit", "seam", "seam_dup", "bwd4", "bwd64", "bwd_dup",
-        "bench512"]
+        "bench512", "pole", "pole64", "pose_rot", "pose_rot64", "pose_pole"]
+
+
+def fixture_pose(fx):
+    """The golden's receiver pose (rotated/offset for the pose_* cases), as
+    the drop-in's ViewPose."""
+    from paper_2511_22793_b200 import ViewPose
+    rx, rot = golden_pose(fx)
+    return ViewPose(rx, rot)
 
 
 @pytest.mark.parametrize("case", GOLD)
-def test_forward_matches_golden(case, R, pose):
+def test_forward_matches_golden(case, R):
     fx = golden(case)
+    pose = fixture_pose(fx)
     cloud = host_cloud(golden_cloud(fx))
     dt = np.dtype(str(fx["dtype"])).type
     img, aux = R.rasterize_forward(cloud, pose, fx["tx"], int(fx["w"]),

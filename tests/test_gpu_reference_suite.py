@@ -1,0 +1,95 @@
+"""The reference's OWN tests, run against the drop-in on the GPU.
+
+SURVEY.md 7 step 4 / 8(b): a user switches backends by rebinding
+`rfsplat.rasterizer` (tests/refsuite_plugin.py); the reference's unmodified
+test files (/root/reference/pkg/tests/test_rasterizer.py and
+test_optimize.py, installed beside the reference in baseline/_ref by
+scripts/install_reference.sh) must then pass with the reference's own
+`GaussianCloud` / `ViewPose` objects flowing into the B200 kernels, and the
+reference's `optimize.train_step` / `train` driving them.
+
+Also acceptance criterion 5 (tests/acceptance5.py) through the device
+trainer and through the reference's own training loop."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+REF_TESTS = os.path.join(REF, "rfsplat_tests")
+
+needs_ref = pytest.mark.skipif(
+    not os.path.isdir(os.path.join(REF, "rfsplat")) or
+    not os.path.isdir(REF_TESTS),
+    reason="reference not installed (scripts/install_reference.sh)")
+
+
+def _env(extra=None):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join(
+        [REF, REF_TESTS, ROOT, os.path.join(ROOT, "tests")] +
+        ([env["PYTHONPATH"]] if env.get("PYTHONPATH") else []))
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    env.update(extra or {})
+    return env
+
+
+def _run_ref_pytest(files, extra_env=None, timeout=1800):
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+           "-p", "refsuite_plugin", "--rootdir", REF_TESTS, "-c", os.devnull,
+           *[os.path.join(REF_TESTS, f) for f in files]]
+    r = subprocess.run(cmd, cwd=REF_TESTS, env=_env(extra_env),
+                       capture_output=True, text=True, timeout=timeout)
+    return r.returncode, r.stdout + r.stderr
+
+
+@needs_ref
+@pytest.mark.parametrize("oracle", ["reference-cpu", "gpu-f64"])
+def test_reference_rasterizer_suite(oracle):
+    """tests/test_rasterizer.py of the reference, every test, unmodified."""
+    rc, out = _run_ref_pytest(
+        ["test_rasterizer.py"],
+        {"REFSUITE_GPU_ORACLE": "1"} if oracle == "gpu-f64" else None)
+    assert "paper_2511_22793_b200 (B200 drop-in)" in out, out[-3000:]
+    assert rc == 0, out[-6000:]
+
+
+@needs_ref
+def test_reference_optimize_suite():
+    """tests/test_optimize.py of the reference: its loss/Adam tests plus
+    train / train_step over the drop-in rasterizer."""
+    rc, out = _run_ref_pytest(["test_optimize.py"])
+    assert rc == 0, out[-6000:]
+
+
+def _acceptance(mode, timeout):
+    r = subprocess.run([sys.executable,
+                        os.path.join(ROOT, "tests", "acceptance5.py"), mode],
+                       env=_env(), capture_output=True, text=True,
+                       timeout=timeout)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-6000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    print(res)
+    return res
+
+
+def test_acceptance5_device_train():
+    """Criterion 5 through paper_2511_22793_b200.optimize.train."""
+    res = _acceptance("device", 900)
+    assert res["final_median"] >= 0.85, res
+    assert res["improvement"] >= 0.30, res
+
+
+@needs_ref
+def test_acceptance5_reference_loop():
+    """Criterion 5 through the reference's own train() (loss, NumPy Adam,
+    PCG64 sampling) with only the rasterizer switched to the drop-in."""
+    res = _acceptance("reference-loop", 1800)
+    assert res["final_median"] >= 0.85, res
+    assert res["improvement"] >= 0.30, res

@@ -5,12 +5,12 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import golden, golden_cloud, golden_dL
+from conftest import golden, golden_cloud, golden_dL, golden_pose
 
 FWD_CASES = ["ka_single", "ka_two", "ka_clamp", "ka_near", "rand96_0",
              "rand96_1", "rand96_2", "f64_noexit", "seam", "seam_dup",
-             "bwd4", "bwd64", "bench512", "bwd_dup"]
-RX, W = np.zeros(3), np.eye(3)
+             "bwd4", "bwd64", "bench512", "bwd_dup", "pole", "pole64",
+             "pose_rot", "pose_rot64", "pose_pole"]
 
 
 def _tiles_src(aux):
@@ -25,6 +25,7 @@ def _tiles_src(aux):
 def test_forward_matches_reference(case):
     fx = golden(case)
     cloud = golden_cloud(fx)
+    RX, W = golden_pose(fx)
     dt = np.dtype(str(fx["dtype"])).type
     img, aux = O.forward(cloud, RX, W, fx["tx"], int(fx["w"]), int(fx["h"]),
                          dtype=dt, t_eps=float(fx["t_eps"]))
@@ -50,6 +51,7 @@ def test_forward_matches_reference(case):
 def test_prepare_matches_reference(case):
     fx = golden(case)
     cloud = golden_cloud(fx)
+    RX, W = golden_pose(fx)
     pr = O.prepare(cloud, RX, W, fx["tx"], int(fx["w"]), int(fx["h"]))
     assert np.array_equal(pr.idx, fx["prep_idx"])
     assert np.array_equal(pr.depth, fx["prep_depth"])
@@ -59,11 +61,17 @@ def test_prepare_matches_reference(case):
         assert np.allclose(got, ref, rtol=1e-13, atol=1e-13), k
 
 
-@pytest.mark.parametrize("case", ["rand96_0", "rand96_1", "rand96_2",
-                                  "bwd4", "bwd64", "bench512", "bwd_dup"])
+RX, W = np.zeros(3), np.eye(3)
+BWD_CASES = ["rand96_0", "rand96_1", "rand96_2", "bwd4", "bwd64",
+             "bench512", "bwd_dup", "pole", "pole64", "pose_rot",
+             "pose_rot64", "pose_pole"]
+
+
+@pytest.mark.parametrize("case", BWD_CASES)
 def test_backward_matches_reference(case):
     fx = golden(case)
     cloud = golden_cloud(fx)
+    RX, W = golden_pose(fx)
     dt = np.dtype(str(fx["dtype"])).type
     _, aux = O.forward(cloud, RX, W, fx["tx"], int(fx["w"]), int(fx["h"]),
                        dtype=dt, t_eps=float(fx["t_eps"]))
