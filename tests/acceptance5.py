@@ -27,7 +27,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-sys.path[:0] = [ROOT, HERE]
+sys.path[:0] = [ROOT, HERE, os.path.join(HERE, "refsuite")]
 
 TRAIN_W, TRAIN_H = 180, 45
 N_GAUSSIANS = 2000

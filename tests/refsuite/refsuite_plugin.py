@@ -28,7 +28,7 @@ import rfsplat.rasterizer as _cpu
 from paper_2511_22793_b200 import rasterizer as _gpu
 
 _shim = types.ModuleType("rfsplat.rasterizer")
-_shim.__doc__ = "B200 drop-in for rfsplat.rasterizer (tests/refsuite_plugin.py)"
+_shim.__doc__ = "B200 drop-in for rfsplat.rasterizer (tests/refsuite/refsuite_plugin.py)"
 for _name in dir(_cpu):
     if not _name.startswith("__"):
         setattr(_shim, _name, getattr(_cpu, _name))
@@ -47,7 +47,16 @@ for _mod in ("rfsplat.optimize", "rfsplat.rfsim", "rfsplat.cli"):
     assert _mod not in sys.modules, f"{_mod} bound the CPU rasterizer early"
 
 
-def pytest_report_header(config):
-    return [f"rfsplat.rasterizer -> {_shim.BACKEND} (B200 drop-in); "
+def _banner():
+    return (f"rfsplat.rasterizer -> {_shim.BACKEND} (B200 drop-in); "
             f"rasterize_reference -> "
-            f"{'GPU f64' if os.environ.get('REFSUITE_GPU_ORACLE') else 'reference CPU'}"]
+            f"{'GPU f64' if os.environ.get('REFSUITE_GPU_ORACLE') else 'reference CPU'}")
+
+
+def pytest_report_header(config):
+    return [_banner()]
+
+
+def pytest_terminal_summary(terminalreporter):
+    # also under -q, where the report header is suppressed
+    terminalreporter.write_line(_banner())

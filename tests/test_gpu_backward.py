@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import golden, golden_cloud, golden_dL, golden_pose
+from conftest import golden, golden_cloud, golden_dL, golden_pose, group_err
 
 pytestmark = pytest.mark.gpu
 
@@ -34,10 +34,6 @@ def host_cloud(oc):
     return GaussianCloud(oc.positions, oc.log_scales, oc.rotations,
                          oc.raw_opacities, oc.mlp_weights, oc.mlp_dims)
 
-
-def group_err(g, ref):
-    return {k: np.abs(np.asarray(g[k]) - ref[k]).max() /
-            max(np.abs(ref[k]).max(), 1e-30) for k in O.GROUPS}
 
 
 def masked_dL(U, flip):

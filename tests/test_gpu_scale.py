@@ -23,6 +23,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from conftest import group_err
 
 pytestmark = pytest.mark.gpu
 
@@ -64,10 +65,6 @@ def tiles_equal(frame_or_aux, aux_ref):
         assert np.array_equal(got[k], want[k]), k
     return sum(len(v) for v in want.values())
 
-
-def group_err(g, ref):
-    return {k: np.abs(np.asarray(g[k]) - ref[k]).max() /
-            max(np.abs(ref[k]).max(), 1e-30) for k in O.GROUPS}
 
 
 def test_config3_full_size_forward():
