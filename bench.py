@@ -581,6 +581,7 @@ def run_ours(args):
     rendered = [torch.cuda.Event() for _ in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
     e2e_steps = min(args.steps, 100)
+    checks = [None, None]
 
     def e2e_run(n):
         for i in range(n):
@@ -589,8 +590,13 @@ def run_ours(args):
             pin_tx[k].copy_(torch.as_tensor(txs_np[t * B:(t + 1) * B]))
             stream.wait_event(copied[k])          # image buffer k is free again
             tx_dev = pin_tx[k].to("cuda", non_blocking=True)
-            out, _ = rasterize_forward_batch(dc, pose, tx_dev, w, h, lazy=lazy,
-                                             frame=frame, image=dev_img[k])
+            # deferred overflow check: verified two renders later, when
+            # buffer k is reused (re-rendered on the rare overflow)
+            if checks[k] is not None and not checks[k].ok():
+                raise RuntimeError("pair buffer overflow in the e2e loop")
+            out, _, checks[k] = rasterize_forward_batch(
+                dc, pose, tx_dev, w, h, lazy=lazy, frame=frame,
+                image=dev_img[k], sync=False)
             rendered[k].record(stream)
             copy_stream.wait_event(rendered[k])
             with torch.cuda.stream(copy_stream):
@@ -669,7 +675,9 @@ def run_ours(args):
                     "d2h_ceiling_gbs": d2h_gbs,
                     "d2h_ceiling_renders_per_s": world * d2h_gbs * 1e9 / img_bytes * B
                     if d2h_gbs else None,
-                    "path": "rasterize_forward_batch(pinned host TX -> device) "
+                    "path": "rasterize_forward_batch(pinned host TX -> device, "
+                            "sync=False: each render's overflow flag read back "
+                            "with it and checked before its buffer is reused) "
                             "+ D2H of every image into pinned memory on a copy "
                             "stream overlapping the next render"},
             "gpu_launches": int(args.steps * per_step_launches),

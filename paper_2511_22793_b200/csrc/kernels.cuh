@@ -19,6 +19,9 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                      int pass, void* img, cudaStream_t st);
 int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                            const void* dL, bool deterministic, cudaStream_t st);
+bool raster_bwd_tc_supported(const gsparc_frame_layout& L, int64_t Cp);
+int launch_raster_bwd_tc(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
+                         const void* dL, bool det, cudaStream_t st);
 int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, const double* tx,
                           int B, const gsparc_frame_layout& L, char* frame, void* grad,
                           int grad_dtype, cudaStream_t st);

@@ -414,10 +414,12 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
       // which (copy, sub-tile) partials exist: K5 wrote those inside each
       // sub-tile's visited prefix (wstop, per 32-pixel warp)
       const int ts = A.tile_start[t];
+      const int wpp = 8 / A.nsub;  // 32-pixel warps (wstop entries) per sub-tile
       unsigned vis = 0;
       for (int copy = 0; copy <= (twice ? 1 : 0); ++copy)
         for (int p = 0; p < A.nsub; ++p) {
-          const int nv = max(A.wstop[t * 8 + p * 2], A.wstop[t * 8 + p * 2 + 1]);
+          int nv = 0;
+          for (int q = 0; q < wpp; ++q) nv = max(nv, A.wstop[t * 8 + p * wpp + q]);
           if (lo + copy - ts < nv) vis |= 1u << (4 * copy + p);
         }
       s_vis[warp][jj] = (unsigned char)vis;
@@ -502,7 +504,12 @@ int launch_raster_backward(const gsparc_frame_layout& L, char* frame, int n_tx, 
     return check_launch("bwd memset");
   }
   int rc;
-  if (L.dtype == GSPARC_F64) {
+  if (raster_bwd_tc_supported(L, A.Cp)) {
+    // both channel contractions on the tensor cores, one CTA per half tile
+    A.nsub = 2;
+    A.nchunks = 1;
+    rc = launch_raster_bwd_tc(L, frame, n_tx, C, dL, det, st);
+  } else if (L.dtype == GSPARC_F64) {
     rc = det ? launch_bwd_cfg<double, 4, 32, true>(A, L.ntiles, st)
              : launch_bwd_cfg<double, 4, 32, false>(A, L.ntiles, st);
   } else if (A.Cp <= 2) {

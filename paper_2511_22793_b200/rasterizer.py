@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .engine import Renderer, dtype_code, split_flat
+from .engine import CapacityError, Renderer, dtype_code, split_flat
 from .geometry import ViewPose
 from .image import SpectrumImage
 from .scene import GROUPS, DeviceCloud, GaussianCloud
@@ -237,15 +237,60 @@ def rasterize_backward(dL_dimage, cloud, pose: ViewPose, tx,
     return ParamGradients(**g)
 
 
+class RenderCheck:
+    """Deferred validity check of an asynchronous batch render (a serving
+    loop's alternative to the per-call host sync): the frame counters are
+    copied to pinned host memory on the render's stream, and `ok()` /
+    `raise_if_overflow()` read them once that copy has landed -- typically
+    when the caller collects the image anyway."""
+
+    RING = 16  # pinned slots per frame: a check stays readable for 16 renders
+
+    def __init__(self, frame):
+        ring = getattr(frame, "_check_ring", None)
+        if ring is None:
+            ring = frame._check_ring = [
+                [torch.empty(_lib.NUM_COUNTERS, dtype=torch.int32,
+                             pin_memory=True), torch.cuda.Event()]
+                for _ in range(self.RING)]
+            frame._check_next = 0
+        self.host, self.event = ring[frame._check_next % self.RING]
+        frame._check_next += 1
+        self.frame = frame
+        self.host.copy_(frame.counters(), non_blocking=True)
+        self.event.record()
+
+    def ok(self):
+        self.event.synchronize()
+        return not int(self.host[_lib.CNT_OVERFLOW])
+
+    def pairs_needed(self):
+        self.event.synchronize()
+        return int(self.host[_lib.CNT_PAIRS])
+
+    def raise_if_overflow(self):
+        if not self.ok():
+            raise CapacityError(self.pairs_needed())
+
+
 def rasterize_forward_batch(cloud: DeviceCloud, pose: ViewPose, txs, w, h,
                             t_eps=T_EPS, lazy=None, with_backward=False,
-                            frame=None, image=None):
+                            frame=None, image=None, sync=True):
     """Render B transmitters at once: image [B, h, w, C] (f32 device tensor)
-    and the frame (device aux) for rasterize_backward_batch."""
+    and the frame (device aux) for rasterize_backward_batch.
+
+    sync=True checks the frame on the host (pair-buffer overflow -> grow and
+    re-render) before returning.  sync=False returns (image, frame,
+    RenderCheck) without waiting for the device; if `check.ok()` is False
+    the image is invalid and the caller re-renders with
+    `renderer().grow(frame, check.pairs_needed())`."""
     txs = _tx_tensor(txs)
     img, frame = renderer().forward(cloud, pose, txs, int(w), int(h),
                                     frame=frame, image=image, t_eps=t_eps,
-                                    lazy=lazy, with_backward=with_backward)
+                                    lazy=lazy, with_backward=with_backward,
+                                    sync_check=sync)
+    if not sync:
+        return img, frame, RenderCheck(frame)
     return img, frame
 
 

@@ -77,16 +77,15 @@ def load(rep, config):
         st = stage_of(d.get("Kernel Name", ""), config)
         if st is None:
             continue
+        # the raw page's second row holds each metric's unit
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         try:
-            b = float(d["dram__bytes_read.sum"].replace(",", "")) + \
-                float(d["dram__bytes_write.sum"].replace(",", ""))
+            b = sum(float(d[m].replace(",", "")) *
+                    scale.get(rows[1][h.index(m)], 1)
+                    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         except (KeyError, ValueError):
             continue
-        # raw page reports bytes in the unit row; ncu --csv gives the unit
-        # in rows[1]
-        unit = rows[1][h.index("dram__bytes_read.sum")]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-        per.setdefault(st, {}).setdefault(d["ID"], {})["dram_bytes"] = b * scale
+        per.setdefault(st, {}).setdefault(d["ID"], {})["dram_bytes"] = b
     out = {}
     for st, launches in per.items():
         keys = set().union(*launches.values())

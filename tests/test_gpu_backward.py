@@ -175,12 +175,16 @@ def test_check_finite(R):
 
 
 @pytest.mark.parametrize("n,F,B", [(1500, 1, 1), (3000, 1, 6), (1200, 4, 2),
-                                   (300, 1, 3)])
+                                   (300, 1, 3),
+                                   # Cp = B*C in [16, 64]: the tensor-core K5
+                                   (2000, 1, 8), (600, 1, 24), (500, 2, 12),
+                                   (800, 1, 32)])
 def test_deterministic_backward(n, F, B, pose):
     """the fixed-order reduction (frame planned with
     with_backward=2) gives bit-identical gradients on every rerun, agrees
     with the atomic accumulation to f32 rounding, and with the oracle's
-    loop-and-sum at the north_star bar."""
+    loop-and-sum at the north_star bar.  Batches of 16..64 channel columns
+    run the tcgen05 backward (raster_bwd_tc.cu), in both modes."""
     import torch
     from paper_2511_22793_b200 import DeviceCloud
     from paper_2511_22793_b200.engine import Renderer, split_flat

@@ -247,3 +247,38 @@ def test_pair_overflow_grow_and_retry(lazy):
         big = R.grow(small, int(fr.counters().cpu()[_lib.CNT_PAIRS]))
         img2, fr2 = R.forward(dc, pose, tx, 360, 90, frame=big, lazy=lazy)
         assert torch.equal(img2, good)
+
+
+def test_async_batch_render_deferred_check():
+    """rasterize_forward_batch(sync=False), the serving-loop form the bench's
+    e2e leg uses: no host sync per call; the RenderCheck read later reports
+    an overflowed frame (so the image is never trusted silently), and a
+    valid frame renders exactly what the synchronous call renders."""
+    import torch
+    from paper_2511_22793_b200 import DeviceCloud, ViewPose
+    from paper_2511_22793_b200.engine import CapacityError
+    from paper_2511_22793_b200.rasterizer import (rasterize_forward_batch,
+                                                  renderer)
+    oc = O.bench_scene(6000, F=26)
+    dc = DeviceCloud.from_host(host_cloud(oc))
+    pose = ViewPose(np.zeros(3))
+    txs = torch.as_tensor(O.sample_tx(4, 3), device="cuda")
+    want, frame = rasterize_forward_batch(dc, pose, txs, 360, 90)
+    want = want.clone()
+    checks = []
+    for _ in range(20):          # more than the pinned ring of 16 slots
+        img, frame, chk = rasterize_forward_batch(dc, pose, txs, 360, 90,
+                                                  frame=frame, sync=False)
+        checks.append(chk)
+    for chk in checks[-16:]:
+        assert chk.ok()
+    assert torch.equal(img, want)
+    small = renderer().new_frame(dc.n, 360, 90, 3 * 52, capacity=1000)
+    _, small, chk = rasterize_forward_batch(dc, pose, txs, 360, 90,
+                                            frame=small, sync=False)
+    assert not chk.ok()
+    with pytest.raises(CapacityError):
+        chk.raise_if_overflow()
+    big = renderer().grow(small, chk.pairs_needed())
+    img2, _ = rasterize_forward_batch(dc, pose, txs, 360, 90, frame=big)
+    assert torch.equal(img2, want)
