@@ -38,10 +38,20 @@ __device__ __forceinline__ int group_of(int64_t e, int64_t n) {
 
 __global__ void k_check_finite(AdamArgs A, int64_t total) {
   int bad = 0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+  // float4 over the flat buffer (group boundaries resolved per element)
+  const int64_t n4 = total >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(A.g);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = g4[q];
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (!isfinite(x[k])) bad |= 1 << group_of(4 * q + k, A.n);
+  }
+  for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const float g = A.g[e];
-    if (!isfinite(g)) bad |= 1 << group_of(e, A.n);
+    if (!isfinite(A.g[e])) bad |= 1 << group_of(e, A.n);
   }
   bad = __reduce_or_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(A.counters + GSPARC_CNT_NONFINITE, bad);
@@ -58,7 +68,19 @@ __device__ double position_lr_dev(double step, const gsparc_adam_config& c) {
   return delay * lr;
 }
 
-__global__ void k_adam(AdamArgs A, int64_t total) {
+__device__ __forceinline__ double adam_upd(double g, float& m, float& v, double lr, double b1,
+                                           double b2, double bc1, double bc2, double eps) {
+  const double mm = b1 * (double)m + (1.0 - b1) * g;
+  const double vv = b2 * (double)v + (1.0 - b2) * g * g;
+  m = (float)mm;
+  v = (float)vv;
+  return lr * (mm / bc1) / (sqrt(vv / bc2) + eps);
+}
+
+// Blocks [0, geo_blocks): thread per Gaussian -- positions, log-scales,
+// rotations (renormalised right after their update, scene.py:117-122) and
+// the opacity; the remaining blocks: the MLP weights, 4 per thread.
+__global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
   // a frame whose pair buffer overflowed produced no valid gradient
   if (A.counters[GSPARC_CNT_NONFINITE] || A.counters[GSPARC_CNT_OVERFLOW]) return;
   // step scalars (pow, exp/log/sin of the position schedule) once per CTA
@@ -73,44 +95,56 @@ __global__ void k_adam(AdamArgs A, int64_t total) {
   __syncthreads();
   const double b1 = A.cfg.beta1, b2 = A.cfg.beta2, eps = A.cfg.eps;
   const double bc1 = s_sc[0], bc2 = s_sc[1];
-  const double lrs[5] = {s_sc[2], A.cfg.scaling_lr, A.cfg.rotation_lr, A.cfg.opacity_lr,
-                         A.cfg.mlp_lr};
   const int64_t n = A.n;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int grp = group_of(e, n);
-    const double g = (double)A.g[e];
-    double m = b1 * (double)A.m[e] + (1.0 - b1) * g;
-    double v = b2 * (double)A.v[e] + (1.0 - b2) * g * g;
-    A.m[e] = (float)m;
-    A.v[e] = (float)v;
-    const double upd = lrs[grp] * (m / bc1) / (sqrt(v / bc2) + eps);
-    switch (grp) {
-      case 0: A.pos[e] -= upd; break;
-      case 1: A.ls[e - 3 * n] -= upd; break;
-      case 2: A.rot[e - 6 * n] -= upd; break;
-      case 3: A.op[e - 10 * n] -= upd; break;
-      default: A.mlp[e - 11 * n] = (float)((double)A.mlp[e - 11 * n] - upd); break;
+  if ((int)blockIdx.x < geo_blocks) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = 0; k < 3; ++k) {
+      const int64_t e = 3 * i + k;
+      A.pos[e] -= adam_upd((double)A.g[e], A.m[e], A.v[e], s_sc[2], b1, b2, bc1, bc2, eps);
     }
+    for (int k = 0; k < 3; ++k) {
+      const int64_t e = 3 * n + 3 * i + k;
+      A.ls[3 * i + k] -=
+          adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.scaling_lr, b1, b2, bc1, bc2, eps);
+    }
+    double q[4];
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = 6 * n + 4 * i + k;
+      q[k] = A.rot[4 * i + k] -
+             adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.rotation_lr, b1, b2, bc1, bc2, eps);
+    }
+    // normalize_quaternions (scene.py:117-122)
+    const double nr = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (nr > 0.0) {
+      for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k] / nr;
+    } else {
+      for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k];
+      atomicOr(A.counters + GSPARC_CNT_NONFINITE, 1 << 5);
+    }
+    {
+      const int64_t e = 10 * n + i;
+      A.op[i] -= adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.opacity_lr, b1, b2, bc1, bc2, eps);
+    }
+    return;
+  }
+  // MLP weights: flat range [11n, total), 4 consecutive elements per thread
+  const int64_t base = 11 * n;
+  const int64_t cnt = total - base;
+  const int64_t q = ((int64_t)blockIdx.x - geo_blocks) * blockDim.x + threadIdx.x;
+  const int64_t e0 = base + 4 * q;
+  if (4 * q >= cnt) return;
+  const double lr = A.cfg.mlp_lr;
+  for (int k = 0; k < 4 && 4 * q + k < cnt; ++k) {
+    const int64_t e = e0 + k;
+    float* w = A.mlp + (e - base);
+    *w = (float)((double)*w - adam_upd((double)A.g[e], A.m[e], A.v[e], lr, b1, b2, bc1, bc2, eps));
   }
 }
 
 __global__ void k_adam_finish(AdamArgs A) {
   const bool skip = A.counters[GSPARC_CNT_NONFINITE] != 0 || A.counters[GSPARC_CNT_OVERFLOW] != 0;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!skip && i < A.n) {  // normalize_quaternions (scene.py:117-122)
-    double* q = A.rot + 4 * i;
-    const double nr = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    if (nr > 0.0) {
-      q[0] /= nr;
-      q[1] /= nr;
-      q[2] /= nr;
-      q[3] /= nr;
-    } else {
-      atomicOr(A.counters + GSPARC_CNT_NONFINITE, 1 << 5);
-    }
-  }
-  if (!skip && i == 0) *A.step += 1;
+  if (!skip) *A.step += 1;
 }
 
 int launch_adam(double* pos, double* ls, double* rot, double* op, float* mlp, int64_t n, int P,
@@ -120,12 +154,15 @@ int launch_adam(double* pos, double* ls, double* rot, double* op, float* mlp, in
   const int64_t total = n * (11 + (int64_t)P);
   if (cudaMemsetAsync(counters + GSPARC_CNT_NONFINITE, 0, sizeof(int), st) != cudaSuccess)
     return check_launch("adam memset");
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  int blocks = (int)((total / 4 + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   k_check_finite<<<blocks, 256, 0, st>>>(A, total);
-  k_adam<<<blocks, 256, 0, st>>>(A, total);
-  k_adam_finish<<<(unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1), 256, 0, st>>>(A);
+  const int geo_blocks = (int)((n + 255) / 256);
+  const int64_t mlp4 = (n * (int64_t)P + 3) / 4;
+  const int mlp_blocks = (int)((mlp4 + 255) / 256);
+  if (geo_blocks + mlp_blocks > 0) k_adam<<<geo_blocks + mlp_blocks, 256, 0, st>>>(A, total, geo_blocks);
+  k_adam_finish<<<1, 1, 0, st>>>(A);
   return check_launch("k_adam");
 }
 

@@ -266,6 +266,215 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
   o[5] = sq0;
 }
 
+// ---------------------------------------------------------------- banded K7
+// Two kernels over (column band of LB output columns, image plane), each
+// staging its band plus a 5-column halo for all rows in shared memory:
+//   k_loss_band_fwd: x/y (|z| for magnitude supervision, reflect-padded
+//     columns) -> h-blur of (x, y, xx, yy, xy) -> v-blur (reflect rows) ->
+//     SSIM and its three adjoint seeds (written to G3) + the band's
+//     fixed-order (ssim, l1, sq) partial sums;
+//   k_loss_band_adj: G3 (zero outside the image) -> adjoint v-blur (rows
+//     folded back at the borders) -> adjoint h-blur (columns folded) ->
+//     L1 term + magnitude chain -> dL/dimg.
+// Same arithmetic (f64, taps in order) as the per-pixel kernels above, two
+// launches instead of six.
+constexpr int LB = 32;  // output columns per band
+
+__host__ __device__ inline int loss_nbands(int w) { return (w + LB - 1) / LB; }
+__host__ __device__ inline size_t loss_band_smem(int h) {
+  return sizeof(double) * (size_t)h * (size_t)(2 * (LB + 10) + 5 * LB);
+}
+__host__ __device__ inline size_t loss_adj_smem(int h) {
+  return sizeof(double) * (size_t)h * (size_t)(6 * (LB + 10));
+}
+constexpr size_t LOSS_SMEM_MAX = 200 * 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
+  extern __shared__ double lsm[];
+  const int h = A.h, w = A.w;
+  const int p = blockIdx.y, b = p / A.S, s = p - b * A.S;
+  const int c0 = blockIdx.x * LB, wc = min(LB, w - c0), XW = wc + 10;
+  double* X = lsm;               // [h][XW]
+  double* Y = X + h * XW;        // [h][XW]
+  double* H5 = Y + h * XW;       // [5][h][wc]
+  for (int e = threadIdx.x; e < h * XW; e += blockDim.x) {
+    const int r = e / XW, cc = e - r * XW;
+    const int col = refl(c0 - 5 + cc, w);
+    X[e] = pred_at(A, b, s, r, col);
+    Y[e] = gt_at(A, b, s, r, col);
+  }
+  __syncthreads();
+  const int HW = h * wc;
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+    const int r = e / wc, c = e - r * wc;
+    double a[5] = {0, 0, 0, 0, 0};
+    const double* xr = X + r * XW + c;
+    const double* yr = Y + r * XW + c;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+      const double x = xr[t], y = yr[t], wt = A.win[t];
+      a[0] += wt * x;
+      a[1] += wt * y;
+      a[2] += wt * (x * x);
+      a[3] += wt * (y * y);
+      a[4] += wt * (x * y);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) H5[k * HW + e] = a[k];
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
+  double v3[3] = {0.0, 0.0, 0.0};
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+    const int r = e / wc, c = e - r * wc;
+    double m[5] = {0, 0, 0, 0, 0};
+    for (int t = 0; t < 11; ++t) {
+      const int rr = refl(r + t - 5, h);
+      const double wt = A.win[t];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) m[k] += wt * H5[k * HW + rr * wc + c];
+    }
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    const double mx = m[0], my = m[1];
+    const double vx = m[2] - mx * mx, vy = m[3] - my * my, vxy = m[4] - mx * my;
+    const double a1 = 2 * mx * my + c1, a2 = 2 * vxy + c2;
+    const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
+    const double sv = (a1 * a2) / (b1 * b2);
+    const double da1 = a2 / (b1 * b2), da2 = a1 / (b1 * b2);
+    const double db1 = -sv / b1, db2 = -sv / b2;
+    const int64_t pe = (int64_t)p * plane + (int64_t)r * w + c0 + c;
+    A.G3[pe] = 2 * my * da1 - 2 * my * da2 + 2 * mx * db1 - 2 * mx * db2;
+    A.G3[tot + pe] = db2;
+    A.G3[2 * tot + pe] = 2 * da2;
+    const double x = X[r * XW + c + 5], y = Y[r * XW + c + 5];
+    v3[0] += sv;
+    v3[1] += fabs(x - y);
+    v3[2] += (x - y) * (x - y);
+  }
+  // fixed-order CTA reduction: warp trees, then warps in order
+  __shared__ double s_part[32][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    v3[k] = warp_sum(v3[k]);
+    if (lane == 0) s_part[warp][k] = v3[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int wq = 0; wq < (int)(blockDim.x >> 5); ++wq) t += s_part[wq][threadIdx.x];
+    A.sums[((int64_t)p * gridDim.x + blockIdx.x) * 3 + threadIdx.x] = t;
+  }
+}
+
+// G(j) = sum_t win[t] g[j + t - 5] over a line held in shared memory whose
+// element q of the image line sits at g[(q - q0) * stride], zero outside
+// [0, n); out(i) = G(i) + [i < 5] G(-i-1) + [i >= n-5] G(2n-1-i)
+template <typename T>
+__device__ __forceinline__ double adj_fold(const LossArgsT<T>& A, const double* g, int stride,
+                                          int q0, int n, int i) {
+  if (i >= 5 && i + 5 < n) {  // interior: all 11 taps in range, no fold-back
+    const double* gi = g + (i - 5 - q0) * stride;
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) acc += A.win[t] * gi[t * stride];
+    return acc;
+  }
+  auto G = [&](int j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+      const int q = j + t - 5;
+      if (q >= 0 && q < n) acc += A.win[t] * g[(q - q0) * stride];
+    }
+    return acc;
+  };
+  double out = G(i);
+  if (i < 5) out += G(-i - 1);
+  if (i >= n - 5) out += G(2 * n - 1 - i);
+  return out;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
+  extern __shared__ double lsm[];
+  const int h = A.h, w = A.w;
+  const int p = blockIdx.y, b = p / A.S, s = p - b * A.S;
+  const int c0 = blockIdx.x * LB, wc = min(LB, w - c0), XW = wc + 10;
+  const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
+  double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+wc+5
+  double* Av = G + 3 * h * XW;     // [3][h][XW]
+  const int HX = h * XW;
+  for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
+    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
+    const int col = c0 - 5 + cc;
+    G[e] = (col >= 0 && col < w) ? A.G3[k * tot + (int64_t)p * plane + (int64_t)r * w + col] : 0.0;
+  }
+  __syncthreads();
+  // adjoint along rows for every staged column (rows complete in smem)
+  for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
+    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
+    Av[e] = adj_fold(A, G + k * HX + cc, XW, 0, h, r);
+  }
+  __syncthreads();
+  const double n = (double)plane;
+  for (int e = threadIdx.x; e < h * wc; e += blockDim.x) {
+    const int r = e / wc, c = e - r * wc, col = c0 + c;
+    const double* row = Av + r * XW;
+    // line index q = image column; element at (q - (c0 - 5))
+    const double amx = adj_fold(A, row, 1, c0 - 5, w, col);
+    const double ab2 = adj_fold(A, row + HX, 1, c0 - 5, w, col);
+    const double aa2 = adj_fold(A, row + 2 * HX, 1, c0 - 5, w, col);
+    const double x = pred_at(A, b, s, r, col), y = gt_at(A, b, s, r, col);
+    const double gssim = (amx + 2 * x * ab2 + y * aa2) / n;
+    const double diff = x - y;
+    const double sgn = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
+    const double gp = (1.0 - A.lam) * sgn / (n * A.S) - A.lam * gssim / A.S;
+    T* dz = A.dimg + (((int64_t)b * h + r) * w + col) * A.C;
+    if (A.sup == 0) {
+      const T* z = A.img + (((int64_t)b * h + r) * w + col) * A.C;
+      const double re = z[0], im = z[1];
+      const double m = hypot(re, im);
+      const double kk = m > 0.0 ? gp / m : 0.0;
+      dz[0] = (T)(re * kk);
+      dz[1] = (T)(im * kk);
+    } else {
+      dz[s] = (T)gp;
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_loss_band_finalize(LossArgsT<T> A, int nbands) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= A.NI) return;
+  const double n = (double)A.h * A.w;
+  double ss = 0.0, l1s = 0.0, sqs = 0.0, ss0 = 0.0, sq0 = 0.0;
+  for (int s = 0; s < A.S; ++s) {
+    const double* sm = A.sums + ((int64_t)b * A.S + s) * nbands * 3;
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < nbands; ++k)
+      for (int q = 0; q < 3; ++q) t[q] += sm[k * 3 + q];
+    ss += t[0] / n;
+    l1s += t[1];
+    sqs += t[2];
+    if (s == 0) {
+      ss0 = t[0] / n;
+      sq0 = t[2] / n;
+    }
+  }
+  ss /= A.S;
+  const double l1 = l1s / (n * A.S);
+  double* o = A.stats + (int64_t)GSPARC_LOSS_STATS * b;
+  o[0] = (1.0 - A.lam) * l1 + A.lam * (1.0 - ss);
+  o[1] = l1;
+  o[2] = ss;
+  o[3] = sqs / (n * A.S);
+  o[4] = ss0;  // channel 0 (optimize.py:281,293)
+  o[5] = sq0;
+}
+
 int64_t loss_scratch_bytes(int NI, int h, int w, int C) {
   const int64_t tot = (int64_t)NI * C * h * w;  // upper bound: S <= C
   return (int64_t)sizeof(double) * (16 * tot + (int64_t)NI * C * 3 * LOSS_RB) + 256;
@@ -298,6 +507,25 @@ static int run_loss(const T* img, const T* gt, int NI, int h, int w, int C, int 
   if (tot >= (int64_t)1 << 31) {
     set_error("loss: %lld pixels x channels exceed 2^31", (long long)tot);
     return GSPARC_ERR_UNSUPPORTED;
+  }
+  if (loss_band_smem(h) <= LOSS_SMEM_MAX && loss_adj_smem(h) <= LOSS_SMEM_MAX) {
+    // banded path: G3 + per-band partial sums in the same scratch
+    const int nb = loss_nbands(w);
+    A.G3 = base;
+    A.sums = base + 3 * tot;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_loss_band_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LOSS_SMEM_MAX);
+      cudaFuncSetAttribute(k_loss_band_adj<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LOSS_SMEM_MAX);
+      attr = true;
+    }
+    const dim3 grid((unsigned)nb, (unsigned)(NI * A.S));
+    k_loss_band_fwd<T><<<grid, 1024, loss_band_smem(h), st>>>(A);
+    k_loss_band_adj<T><<<grid, 1024, loss_adj_smem(h), st>>>(A);
+    k_loss_band_finalize<T><<<(NI + 127) / 128, 128, 0, st>>>(A, nb);
+    return check_launch("k_loss_band");
   }
   const unsigned blocks = (unsigned)((tot + 255) / 256);
   k_loss_prep<T><<<blocks, 256, 0, st>>>(A);

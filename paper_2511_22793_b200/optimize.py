@@ -282,8 +282,8 @@ class Trainer:
         self.graph = None
 
     def _gather(self):
-        self.tx.copy_(self.tx_all.index_select(0, self.idx))
-        self.gt.copy_(self.gt_all.index_select(0, self.idx))
+        torch.index_select(self.tx_all, 0, self.idx, out=self.tx)
+        torch.index_select(self.gt_all, 0, self.idx, out=self.gt)
 
     def _compute(self):
         self.R.forward(self.dev, self.pose, self.tx, self.w, self.h,
