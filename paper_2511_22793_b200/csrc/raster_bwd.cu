@@ -431,18 +431,27 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
       const int64_t cc = c0 + lane;
       if (cc < A.Cp) {
         R acc = R(0);
-        for (int jj = 0; jj < nj; ++jj) {
-          const int64_t k0 = s_pos[warp][jj];
-          const unsigned vis = s_vis[warp][jj];
-          R v[8];
+        // 4 slots' partials in flight per round (the sum stays in slot order)
+        for (int jb = 0; jb < nj; jb += 4) {
+          R v[4][8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            v[q] = ((vis >> q) & 1u)
-                       ? dgc[((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.Cp + cc]
-                       : R(0);
+          for (int u = 0; u < 4; ++u) {
+            const int jj = jb + u;
+            const unsigned vis = jj < nj ? s_vis[warp][jj] : 0u;
+            const int64_t k0 = jj < nj ? s_pos[warp][jj] : 0;
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if ((vis >> q) & 1u) acc += v[q];
+            for (int q = 0; q < 8; ++q)
+              v[u][q] = ((vis >> q) & 1u)
+                            ? dgc[((k0 + (q >> 2)) * A.nsub + (q & 3)) * A.Cp + cc]
+                            : R(0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned vis = jb + u < nj ? s_vis[warp][jb + u] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if ((vis >> q) & 1u) acc += v[u][q];
+          }
         }
         gc[cc] = j0 == 0 ? acc : gc[cc] + acc;
       }
