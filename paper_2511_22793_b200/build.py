@@ -63,7 +63,14 @@ def _compile(src, hdr, force):
     return obj
 
 
-def build(force=False, verbose=True):
+def build(force=False, verbose=True, experiments=False):
+    """experiments=True compiles the timing/tuning environment knobs in
+    (-DGSPARC_EXPERIMENTS, common.cuh experiment_env); the default product
+    build ignores them."""
+    global FLAGS
+    FLAGS = [f for f in FLAGS if f != "-DGSPARC_EXPERIMENTS"]
+    if experiments:
+        FLAGS = FLAGS + ["-DGSPARC_EXPERIMENTS"]
     os.makedirs(OBJ, exist_ok=True)
     hdr = _headers_digest()
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
@@ -82,4 +89,7 @@ def build(force=False, verbose=True):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
-    build(force=ap.parse_args().force)
+    ap.add_argument("--experiments", action="store_true",
+                    help="compile in the GSPARC_* experiment knobs")
+    a = ap.parse_args()
+    build(force=a.force, experiments=a.experiments)

@@ -537,7 +537,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st,
   A.ntx = L.ntx;
   A.ntiles = L.ntiles;
   A.dbg = nullptr;
-  if (getenv("GSPARC_SORT_DBG")) A.dbg = dbg_rows(0);  // experiments only
+  if (experiment_env("GSPARC_SORT_DBG")) A.dbg = dbg_rows(0);  // experiments only
   const size_t cnt_ints =
       (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + RS_W + 2 + 3 * SEG_MAX + 1);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;
@@ -553,7 +553,7 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st,
   // dependent launch behind K2 on the lazy render path (config 3: -0.5 us);
   // ahead of the full MLP (config 1) it measured 5 us slower, so there the
   // sort is an ordinary launch (griddepcontrol.wait then returns at once)
-  static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K3");
+  static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !experiment_env("GSPARC_NO_PDL_K3");
   const bool pdl = pdl_env && dependent;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];

@@ -13,6 +13,7 @@
 //   tile lists: tile_start[T+1] (exclusive scan) and pairs[] u64
 //     = (coarse_depth32 << 32) | source_index, sorted per tile.
 #pragma once
+#include <stdlib.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -300,6 +301,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------- host side
+// Tuning / timing knobs of the experiments (scripts/ab_env.sh, dbg_*.py) are
+// read from the environment only in builds with -DGSPARC_EXPERIMENTS
+// (python -m paper_2511_22793_b200.build --experiments); the product build
+// always runs the defaults.  The two test hooks that select an equivalent
+// code path (GSPARC_NO_PDL: stream-ordered launches; GSPARC_PXW_CHUNKS: the
+// pass-B weight recompute) are read directly with getenv.
+inline const char* experiment_env(const char* name) {
+#ifdef GSPARC_EXPERIMENTS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 

@@ -221,7 +221,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
                const gsparc_frame_layout& L, char* frame, cudaStream_t st, int stream_ctas) {
   MlpArgs A;
   A.stream_ctas = 0;
-  A.dbg = getenv("GSPARC_MLP_DBG") ? dbg_rows(3) + 16 * 2048 : nullptr;  // experiments only
+  A.dbg = experiment_env("GSPARC_MLP_DBG") ? dbg_rows(3) + 16 * 2048 : nullptr;  // experiments only
   A.w32 = cloud.mlp_weights;
   A.w64 = cloud.mlp_weights64;
   A.pos = cloud.positions;
@@ -264,7 +264,7 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     // renders have fewer live Gaussians than resident warps
     if (live_only && blocks > 148 * 2) blocks = 148 * 2;
     static const int stream_blocks =
-        getenv("GSPARC_MLP_SBLOCKS") ? atoi(getenv("GSPARC_MLP_SBLOCKS")) : 148;
+        experiment_env("GSPARC_MLP_SBLOCKS") ? atoi(experiment_env("GSPARC_MLP_SBLOCKS")) : 148;
     if (live_only && stream_ctas > 0 && !getenv("GSPARC_NO_PDL")) {
       // one CTA per SM: all resident next to pass A's two CTAs, so no entry
       // waits for a CTA that can only start when pass A leaves

@@ -449,15 +449,15 @@ int launch_preprocess(const gsparc_cloud& cloud, const gsparc_view& view,
   A.seg = (int2*)(frame + L.off_seg);
   A.capacity = L.pair_capacity;
   A.seg_stride = (int)L.seg_stride;
-  A.dbg = getenv("GSPARC_PREP_DBG") ? dbg_rows(3) : nullptr;  // experiments only
-  A.bin_small = getenv("GSPARC_BIN_SMALL") ? atoi(getenv("GSPARC_BIN_SMALL")) : 40;
+  A.dbg = experiment_env("GSPARC_PREP_DBG") ? dbg_rows(3) : nullptr;  // experiments only
+  A.bin_small = experiment_env("GSPARC_BIN_SMALL") ? atoi(experiment_env("GSPARC_BIN_SMALL")) : 40;
   // counters | tile_count | tile_cursor are laid out back to back
   const int64_t zero_end = L.off_tile_cursor + (int64_t)sizeof(int) * L.ntiles;
   if (L.off_tile_count < L.off_counters || L.off_tile_cursor < L.off_tile_count) {
     set_error("preprocess: unexpected frame layout");
     return GSPARC_ERR_ARG;
   }
-  static const bool pdl = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_K2");
+  static const bool pdl = !getenv("GSPARC_NO_PDL") && !experiment_env("GSPARC_NO_PDL_K2");
   if (pdl) {
     const int nz = (int)((zero_end - L.off_counters) / (int64_t)sizeof(int));
     k_clear_frame<<<1, 256, 0, st>>>((int*)(frame + L.off_counters), nz);

@@ -933,17 +933,17 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   // top/bottom interleave: measured on the render path with one channel
   // chunk (config 3: 105.8 -> 104.7 us); with a dependent launch (config 5)
   // or behind pass A (config 1) it was 1-2% slower, so it is off there
-  static const int mix = getenv("GSPARC_PXB_MIX") ? atoi(getenv("GSPARC_PXB_MIX")) : -1;
+  static const int mix = experiment_env("GSPARC_PXB_MIX") ? atoi(experiment_env("GSPARC_PXB_MIX")) : -1;
   B.mix_b = mix >= 0 ? mix : (after_mlp && chunks_y == 1);
-  if (getenv("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
+  if (experiment_env("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   // dependent launch behind the streaming MLP (render path, pass 2): the
   // prologue (TMEM allocation, barriers, stage clearing) overlaps the MLP's
   // tail.  Measured: config 5 +4.7%, config 3 neutral; directly behind pass
   // A (pass 0) the early CTAs only park on the SMs (config 1 -2.5%).
-  static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !getenv("GSPARC_NO_PDL_B");
+  static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !experiment_env("GSPARC_NO_PDL_B");
   // (one channel chunk, e.g. config 3: an ordinary launch with the reads
   // ahead of the prologue is as fast)
-  static const bool pdl1 = getenv("GSPARC_PXB_PDL1") != nullptr;  // experiments
+  static const bool pdl1 = experiment_env("GSPARC_PXB_PDL1") != nullptr;  // experiments
   const bool pdl = pdl_env && after_mlp && (chunks_y > 1 || pdl1);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -1008,7 +1008,7 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
                      int pass, void* img, cudaStream_t st) {
   PxArgs A = make_px_args(L, frame, n_tx, C, t_eps, img);
   const int64_t Cp = A.Cp;
-  if (pass != 2 && getenv("GSPARC_PXA_DBG")) {  // experiments only: pass-A timing
+  if (pass != 2 && experiment_env("GSPARC_PXA_DBG")) {  // experiments only: pass-A timing
     A.dbg = dbg_rows(1);
   }
   if (pass != 2) {
@@ -1028,14 +1028,14 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
     // two pass-A CTAs per SM at most (a shared-memory reservation): CTAs
     // that start while K3 still runs would otherwise pile up four to an SM
     // on the first free SMs and run the heaviest tiles at half speed
-    static const int pad_kb = getenv("GSPARC_PXA_SMEM") ? atoi(getenv("GSPARC_PXA_SMEM")) : 90;
+    static const int pad_kb = experiment_env("GSPARC_PXA_SMEM") ? atoi(experiment_env("GSPARC_PXA_SMEM")) : 90;
     if (pdl && pad_kb > 0) {
       static bool attr = false;
       if (!attr) {
         const void* ks[5] = {(const void*)k_pxa<0>, (const void*)k_pxa<1>, (const void*)k_pxa<2>,
                              (const void*)k_pxa<3>, (const void*)k_pxa<4>};
         static const int carve =
-            getenv("GSPARC_PXA_CARVE") ? atoi(getenv("GSPARC_PXA_CARVE")) : 100;
+            experiment_env("GSPARC_PXA_CARVE") ? atoi(experiment_env("GSPARC_PXA_CARVE")) : 100;
         for (const void* k : ks) {
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pad_kb * 1024);
           cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
