@@ -9,6 +9,8 @@
 //   mlp_weights(n,P)
 // (the ParamGradients groups of rasterizer.py:39-61), overwriting it.
 // Culled Gaussians get exact zeros.  TX batches sum their gradients.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -40,7 +42,7 @@ __device__ __forceinline__ void put(G* base, int64_t k, double v) {
 
 // FR: frame / weight precision (float or double); G: gradient dtype.
 template <typename FR, typename G>
-__global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
+__global__ void __launch_bounds__(128, 4) k_gauss_bwd(GBwdArgs A) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -95,71 +97,76 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
     // the weight gradients sum_b gpre_b (x) x_b, gs_b (x) hid_b are then
     // 32-term dots over the lanes' rows staged in shared memory, owned by
     // lane e (mod 32) of the flat parameter row, accumulated in registers.
+    // MT: f32 for the training path (f32 frame and gradients: the sums run
+    // over <= 32 TX, ~1e-7 relative), f64 otherwise (the drop-in's f64
+    // gradients follow the reference's f64 mlp.batch_mlp_backward)
+    using MT = std::conditional_t<sizeof(FR) == 4 && sizeof(G) == 4, float, double>;
     constexpr int H16 = 16, I5 = 5, JMAX = LANE_TX_JMAX;
-    double* t_gp = sw;                      // [32][17] dL/d pre
-    double* t_hid = t_gp + 32 * (H16 + 1);  // [32][17] hidden
-    double* t_x = t_hid + 32 * (H16 + 1);   // [32][6]  inputs
-    double* t_gs = t_x + 32 * (I5 + 1);     // [32][C+1] dL/d s
+    MT* t_gp = reinterpret_cast<MT*>(smraw) +
+               (size_t)warp * 32 * (2 * (H16 + 1) + I5 + 1 + C + 1);  // [32][17] dL/d pre
+    MT* t_hid = t_gp + 32 * (H16 + 1);  // [32][17] hidden
+    MT* t_x = t_hid + 32 * (H16 + 1);   // [32][6]  inputs
+    MT* t_gs = t_x + 32 * (I5 + 1);     // [32][C+1] dL/d s
     const int CP1 = C + 1;
-    double acc[JMAX];
+    MT acc[JMAX];
 #pragma unroll
-    for (int j = 0; j < JMAX; ++j) acc[j] = 0.0;
-    double gth = 0.0, gph = 0.0, gq0 = 0.0, gq1 = 0.0, gq2 = 0.0;
+    for (int j = 0; j < JMAX; ++j) acc[j] = MT(0);
+    MT gth = 0, gph = 0, gq0 = 0, gq1 = 0, gq2 = 0;
     for (int b0 = 0; b0 < A.B; b0 += 32) {
       const int b = b0 + lane;
       const bool vb = b < A.B;
-      double x[I5], hid[H16], gh[H16];
-      x[3] = theta;
-      x[4] = phi;
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, draw = 1.0, d = 1.0;
+      MT x[I5], hid[H16], gh[H16];
+      x[3] = (MT)theta;
+      x[4] = (MT)phi;
+      MT d0 = 0, d1 = 0, d2 = 0, draw = 1, d = 1;
       if (vb) {
         const double* txb = A.tx + 3 * b;
-        x[0] = (double)(FR)txb[0];
-        x[1] = (double)(FR)txb[1];
-        x[2] = (double)(FR)txb[2];
-        d0 = pos[0] - txb[0];
-        d1 = pos[1] - txb[1];
-        d2 = pos[2] - txb[2];
+        x[0] = (MT)(FR)txb[0];
+        x[1] = (MT)(FR)txb[1];
+        x[2] = (MT)(FR)txb[2];
+        d0 = (MT)(pos[0] - txb[0]);
+        d1 = (MT)(pos[1] - txb[1]);
+        d2 = (MT)(pos[2] - txb[2]);
         draw = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-        d = draw < NEAR_PLANE ? NEAR_PLANE : draw;
+        d = draw < (MT)NEAR_PLANE ? (MT)NEAR_PLANE : draw;
       } else {
-        x[0] = x[1] = x[2] = 0.0;
+        x[0] = x[1] = x[2] = MT(0);
       }
 #pragma unroll
       for (int h = 0; h < H16; ++h) {
-        double v = 0.0;
+        MT v = 0;
 #pragma unroll
-        for (int k = 0; k < I5; ++k) v += (double)W1[h * I5 + k] * x[k];
-        v += (double)b1[h];
-        hid[h] = v > 0.0 ? v : 0.0;
-        gh[h] = 0.0;
+        for (int k = 0; k < I5; ++k) v += (MT)W1[h * I5 + k] * x[k];
+        v += (MT)b1[h];
+        hid[h] = v > MT(0) ? v : MT(0);
+        gh[h] = 0;
       }
-      double gd_part = 0.0;
+      MT gd_part = 0;
       for (int c = 0; c < C; ++c) {
-        double sc = 0.0;
+        MT sc = 0;
 #pragma unroll
-        for (int h = 0; h < H16; ++h) sc += (double)W2[c * H16 + h] * hid[h];
-        sc += (double)b2[c];
-        const double gcv = vb ? (double)gcoef[(int64_t)b * C + c] : 0.0;
-        const double gsc = gcv / d;
+        for (int h = 0; h < H16; ++h) sc += (MT)W2[c * H16 + h] * hid[h];
+        sc += (MT)b2[c];
+        const MT gcv = vb ? (MT)gcoef[(int64_t)b * C + c] : MT(0);
+        const MT gsc = gcv / d;
         gd_part -= gcv * sc;
 #pragma unroll
-        for (int h = 0; h < H16; ++h) gh[h] += (double)W2[c * H16 + h] * gsc;
+        for (int h = 0; h < H16; ++h) gh[h] += (MT)W2[c * H16 + h] * gsc;
         t_gs[lane * CP1 + c] = gsc;
       }
-      const double g_d = gd_part / (d * d);
-      if (vb && !(draw < NEAR_PLANE)) {  // rasterizer.py:366-368
+      const MT g_d = gd_part / (d * d);
+      if (vb && !(draw < (MT)NEAR_PLANE)) {  // rasterizer.py:366-368
         gq0 += g_d * d0 / d;
         gq1 += g_d * d1 / d;
         gq2 += g_d * d2 / d;
       }
 #pragma unroll
       for (int h = 0; h < H16; ++h) {
-        const double gp = hid[h] > 0.0 ? gh[h] : 0.0;  // relu' (pre > 0 <=> hid > 0)
-        gth += (double)W1[h * I5 + 3] * gp;
-        gph += (double)W1[h * I5 + 4] * gp;
+        const MT gp = hid[h] > MT(0) ? gh[h] : MT(0);  // relu' (pre > 0 <=> hid > 0)
+        gth += (MT)W1[h * I5 + 3] * gp;
+        gph += (MT)W1[h * I5 + 4] * gp;
         t_gp[lane * (H16 + 1) + h] = gp;
-        t_hid[lane * (H16 + 1) + h] = vb ? hid[h] : 0.0;
+        t_hid[lane * (H16 + 1) + h] = vb ? hid[h] : MT(0);
       }
 #pragma unroll
       for (int k = 0; k < I5; ++k) t_x[lane * (I5 + 1) + k] = x[k];
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(128) k_gauss_bwd(GBwdArgs A) {
       for (int j = 0; j < JMAX; ++j) {
         const int e = lane + 32 * j;
         if (e >= P) break;
-        double v = 0.0;
+        MT v = 0;
         if (e < H16 * I5) {
           const int h = e / I5, k = e - h * I5;
           for (int l = 0; l < nl; ++l) v += t_gp[l * (H16 + 1) + h] * t_x[l * (I5 + 1) + k];
@@ -493,7 +500,10 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
   const size_t per_warp =
       A.lane_tx ? (size_t)32 * (2 * 17 + 6 + cloud.mlp_out + 1)
                 : (size_t)(8 + 96 + cloud.mlp_out + A.P);
-  const size_t smem = sizeof(double) * (threads / 32) * per_warp;
+  // the lane-per-TX path stages f32 rows for f32 frames and gradients
+  const size_t elem = (A.lane_tx && L.dtype == GSPARC_F32 && grad_dtype == GSPARC_F32)
+                          ? sizeof(float) : sizeof(double);
+  const size_t smem = elem * (threads / 32) * per_warp;
   if (smem > 227 * 1024) {
     set_error("gaussian backward: %d MLP parameters exceed shared memory", A.P);
     return GSPARC_ERR_UNSUPPORTED;
