@@ -44,6 +44,47 @@ __device__ __forceinline__ double tx_distance(const double* pos, const double* t
   return d < NEAR_PLANE ? NEAR_PLANE : d;  // rasterizer.py:103-105
 }
 
+// (5, 16, C) head with few outputs (C <= 8, e.g. the 2-channel RSSI model
+// batched over TX): thread per (Gaussian, TX), a warp = one Gaussian's
+// weights (broadcast loads) for 32 transmitters; loops unrolled, hidden layer
+// in registers.
+template <int C>
+__global__ void __launch_bounds__(256) k_mlp_narrow516(MlpArgs A) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gi = t / A.B;
+  const int b = (int)(t % A.B);
+  const int64_t count = A.live_list ? A.counters[GSPARC_CNT_LIVE] : A.n;
+  if (gi >= count) return;
+  const int64_t i = A.live_list ? A.live_list[gi] : gi;
+  if (!A.live_list && A.key[i] == ~0ULL) return;
+  const float4 r = A.rec32[2 * i + 1];
+  const double* txb = A.tx + 3 * b;
+  const float x[5] = {(float)txb[0], (float)txb[1], (float)txb[2], r.z, r.w};
+  constexpr int H = 16, I = 5;
+  const float* w = A.w32 + i * (int64_t)A.P;
+  float hid[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < I; ++k) acc += w[h * I + k] * x[k];
+    acc += w[H * I + h];
+    hid[h] = acc > 0.f ? acc : 0.f;
+  }
+  const float* w2 = w + H * I + H;
+  const float* b2 = w2 + C * H;
+  const double d = tx_distance(A.pos + 3 * i, txb);
+  float* out = (float*)A.coef + i * A.Cp + (int64_t)b * C;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    float acc = 0.f;
+#pragma unroll
+    for (int h = 0; h < H; ++h) acc += w2[c * H + h] * hid[h];
+    acc += b2[c];
+    out[c] = (float)((double)acc / d);
+  }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(256) k_mlp_narrow(MlpArgs A) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,7 +328,16 @@ int launch_mlp(const gsparc_cloud& cloud, const double* tx, int B, bool live_onl
     }
   } else {
     int64_t threads = cloud.n * B;
-    k_mlp_narrow<float><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(A);
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    if (A.H == 16 && A.I == 5 && A.C == 2) {
+      k_mlp_narrow516<2><<<blocks, 256, 0, st>>>(A);
+    } else if (A.H == 16 && A.I == 5 && A.C == 4) {
+      k_mlp_narrow516<4><<<blocks, 256, 0, st>>>(A);
+    } else if (A.H == 16 && A.I == 5 && A.C == 8) {
+      k_mlp_narrow516<8><<<blocks, 256, 0, st>>>(A);
+    } else {
+      k_mlp_narrow<float><<<blocks, 256, 0, st>>>(A);
+    }
   }
   return check_launch("k_mlp");
 }
