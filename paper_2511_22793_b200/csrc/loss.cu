@@ -280,6 +280,20 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
 // launches instead of six.
 constexpr int LB = 32;  // output columns per band
 
+// q = e / d for the small non-negative ranges of the band loops (e < 2^22)
+// without the ~20-instruction integer division: float estimate + fix-up
+struct FastDiv {
+  int d;
+  float inv;
+  __device__ FastDiv(int d_) : d(d_), inv(1.0f / (float)d_) {}
+  __device__ __forceinline__ int div(int e) const {
+    int q = __float2int_rz((float)e * inv);
+    const int r = e - q * d;
+    q += (r >= d) - (r < 0);
+    return q;
+  }
+};
+
 __host__ __device__ inline int loss_nbands(int w) { return (w + LB - 1) / LB; }
 __host__ __device__ inline size_t loss_band_smem(int h) {
   return sizeof(double) * (size_t)h * (size_t)(2 * (LB + 10) + 5 * LB);
@@ -298,8 +312,11 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   double* X = lsm;               // [h][XW]
   double* Y = X + h * XW;        // [h][XW]
   double* H5 = Y + h * XW;       // [5][h][wc]
+  // loads of several elements in flight per thread before the stores
+  const FastDiv dXW(XW), dWC(wc);
+#pragma unroll 4
   for (int e = threadIdx.x; e < h * XW; e += blockDim.x) {
-    const int r = e / XW, cc = e - r * XW;
+    const int r = dXW.div(e), cc = e - r * XW;
     const int col = refl(c0 - 5 + cc, w);
     X[e] = pred_at(A, b, s, r, col);
     Y[e] = gt_at(A, b, s, r, col);
@@ -307,7 +324,7 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   __syncthreads();
   const int HW = h * wc;
   for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = e / wc, c = e - r * wc;
+    const int r = dWC.div(e), c = e - r * wc;
     double a[5] = {0, 0, 0, 0, 0};
     const double* xr = X + r * XW + c;
     const double* yr = Y + r * XW + c;
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
   double v3[3] = {0.0, 0.0, 0.0};
   for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = e / wc, c = e - r * wc;
+    const int r = dWC.div(e), c = e - r * wc;
     double m[5] = {0, 0, 0, 0, 0};
     for (int t = 0; t < 11; ++t) {
       const int rr = refl(r + t - 5, h);
@@ -340,9 +357,12 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
     const double vx = m[2] - mx * mx, vy = m[3] - my * my, vxy = m[4] - mx * my;
     const double a1 = 2 * mx * my + c1, a2 = 2 * vxy + c2;
     const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
-    const double sv = (a1 * a2) / (b1 * b2);
-    const double da1 = a2 / (b1 * b2), da2 = a1 / (b1 * b2);
-    const double db1 = -sv / b1, db2 = -sv / b2;
+    // one f64 division per pixel instead of five (1/(b1 b2) and its
+    // products give 1/b1 = b2 / (b1 b2), 1/b2 = b1 / (b1 b2))
+    const double ib = 1.0 / (b1 * b2);
+    const double sv = (a1 * a2) * ib;
+    const double da1 = a2 * ib, da2 = a1 * ib;
+    const double db1 = -sv * (b2 * ib), db2 = -sv * (b1 * ib);
     const int64_t pe = (int64_t)p * plane + (int64_t)r * w + c0 + c;
     A.G3[pe] = 2 * my * da1 - 2 * my * da2 + 2 * mx * db1 - 2 * mx * db2;
     A.G3[tot + pe] = db2;
@@ -406,31 +426,34 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
   double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+wc+5
   double* Av = G + 3 * h * XW;     // [3][h][XW]
   const int HX = h * XW;
+  const FastDiv dHX(HX), dXW(XW), dWC(wc);
+#pragma unroll 4
   for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
+    const int k = dHX.div(e), rem = e - k * HX, r = dXW.div(rem), cc = rem - r * XW;
     const int col = c0 - 5 + cc;
     G[e] = (col >= 0 && col < w) ? A.G3[k * tot + (int64_t)p * plane + (int64_t)r * w + col] : 0.0;
   }
   __syncthreads();
   // adjoint along rows for every staged column (rows complete in smem)
   for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
+    const int k = dHX.div(e), rem = e - k * HX, r = dXW.div(rem), cc = rem - r * XW;
     Av[e] = adj_fold(A, G + k * HX + cc, XW, 0, h, r);
   }
   __syncthreads();
   const double n = (double)plane;
+  const double inv_n = 1.0 / n, k_l1 = (1.0 - A.lam) / (n * A.S), k_ss = A.lam / A.S;
   for (int e = threadIdx.x; e < h * wc; e += blockDim.x) {
-    const int r = e / wc, c = e - r * wc, col = c0 + c;
+    const int r = dWC.div(e), c = e - r * wc, col = c0 + c;
     const double* row = Av + r * XW;
     // line index q = image column; element at (q - (c0 - 5))
     const double amx = adj_fold(A, row, 1, c0 - 5, w, col);
     const double ab2 = adj_fold(A, row + HX, 1, c0 - 5, w, col);
     const double aa2 = adj_fold(A, row + 2 * HX, 1, c0 - 5, w, col);
     const double x = pred_at(A, b, s, r, col), y = gt_at(A, b, s, r, col);
-    const double gssim = (amx + 2 * x * ab2 + y * aa2) / n;
+    const double gssim = (amx + 2 * x * ab2 + y * aa2) * inv_n;
     const double diff = x - y;
     const double sgn = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
-    const double gp = (1.0 - A.lam) * sgn / (n * A.S) - A.lam * gssim / A.S;
+    const double gp = sgn * k_l1 - k_ss * gssim;
     T* dz = A.dimg + (((int64_t)b * h + r) * w + col) * A.C;
     if (A.sup == 0) {
       const T* z = A.img + (((int64_t)b * h + r) * w + col) * A.C;
