@@ -1065,7 +1065,11 @@ int launch_raster_px(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
     A.ready = nullptr;
     if (pass == 1) return GSPARC_OK;
   }
-  const int chunks = (int)((Cp + 255) / 256);
+  // wide batches (> 256 columns, e.g. config 5's 2048) in 128-column chunks:
+  // two CTAs per SM (256 TMEM columns each) hide the coef-row load latency
+  // that a 256-column CTA alone on its SM waits on
+  const int np_max = Cp > 256 ? 128 : 256;
+  const int chunks = (int)((Cp + np_max - 1) / np_max);
   const int64_t per = (Cp + chunks - 1) / chunks;
   const bool after_mlp = pass == 2;
   if (per <= 32) launch_pxb<32>(A, chunks, after_mlp, st);
