@@ -458,7 +458,31 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
     }
     if (lane < 8) {
       R acc = R(0);
-      if (lane < 6) {
+      if (lane < 6 && A.nchunks == 1) {
+        // one channel chunk: 4 slots' partials in flight per round, summed
+        // in the same (slot, copy/sub-tile) order as the general loop
+        for (int jb = 0; jb < nj; jb += 4) {
+          R v[4][8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int jj = jb + u;
+            const unsigned vis = jj < nj ? s_vis[warp][jj] : 0u;
+            const int64_t k0 = jj < nj ? s_pos[warp][jj] : 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              v[u][q] = ((vis >> q) & 1u)
+                            ? dgg[((k0 + (q >> 2)) * A.nsub + (q & 3)) * 6 + lane]
+                            : R(0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned vis = jb + u < nj ? s_vis[warp][jb + u] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if ((vis >> q) & 1u) acc += v[u][q];
+          }
+        }
+      } else if (lane < 6) {
         for (int jj = 0; jj < nj; ++jj) {
           const int64_t k0 = s_pos[warp][jj];
           const unsigned vis = s_vis[warp][jj];
