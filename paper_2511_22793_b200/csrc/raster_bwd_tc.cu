@@ -19,10 +19,10 @@
 // Only the sequential back-to-front scan (alpha, T, the suffix sum, the
 // geometric gradients of rasterizer.py:302-321) stays on the CUDA cores.
 //
-// Warp roles (256 threads, one CTA per half tile):
+// Warp roles (320 threads, one CTA per half tile):
 //   0-3  scan: pixel per lane (TMEM lane quadrant = warp), 32 entries per
 //        batch fully unrolled; warp-reduced geometric gradients
-//   4-5  GEMM-2 epilogue: lane = channel, 32 entries per tcgen05.ld
+//   4-5, 8-9  GEMM-2 epilogue: lane = channel, 16 entries each per tcgen05.ld
 //   6    loader: the batch's list entries, raster records and coef rows
 //        (split hi/lo, swizzled) one batch ahead
 //   7    MMA issuer (one thread): GEMM 1 of batch b+1 before GEMM 2 of b
@@ -131,20 +131,18 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];
@@ -207,7 +205,7 @@ struct BwdTcArgs {
   int det;
 };
 
-__global__ void __launch_bounds__(256, 1) k_raster_bwd_tc(BwdTcArgs A) {
+__global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   __shared__ TcShared S;
@@ -237,9 +235,9 @@ __global__ void __launch_bounds__(256, 1) k_raster_bwd_tc(BwdTcArgs A) {
       bar_init(&S.w_full[k], 4);
       bar_init(&S.w_empty[k], 1);
       bar_init(&S.d2_full[k], 1);
-      bar_init(&S.d2_empty[k], 2);
+      bar_init(&S.d2_empty[k], 4);
       bar_init(&S.red_full[k], 4);
-      bar_init(&S.red_empty[k], 2);
+      bar_init(&S.red_empty[k], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -429,7 +427,10 @@ __global__ void __launch_bounds__(256, 1) k_raster_bwd_tc(BwdTcArgs A) {
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ GEMM-2 epilogue
-    const int c = 32 * (warp - 4) + lane;  // channel = TMEM lane
+    // warps 4, 5, 8, 9: TMEM lane quadrant qe = warp % 4 (channels 32 qe ..),
+    // entry half eh (entries 16 eh .. 16 eh + 15 of each batch)
+    const int qe = warp & 3, eh = warp >= 8 ? 1 : 0, ew = 2 * eh + qe;
+    const int c = 32 * qe + lane;  // channel = TMEM lane
     for (int b = 0; b < nbatch; ++b) {
       const int g = b & 1;
       int b0, nb;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(256, 1) k_raster_bwd_tc(BwdTcArgs A) {
       bar_wait_sleep(&S.red_full[g], (b >> 1) & 1);
       {
         const float (*red)[4][6] = S.red[g];
-        for (int e = 32 * (warp - 4) + lane; e < TC_NB * 6; e += 64) {
+        for (int e = 32 * ew + lane; e < TC_NB * 6; e += 128) {
           const int j = e / 6, f = e - j * 6;
           const int sj = __shfl_sync(0xffffffffu, myidx, j);
           if (j < nb) {
@@ -467,17 +468,18 @@ __global__ void __launch_bounds__(256, 1) k_raster_bwd_tc(BwdTcArgs A) {
       // (2) dL/dcoef rows from GEMM 2
       bar_wait_sleep(&S.d2_full[g], (b >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * (warp - 4)) << 16) + COL_D2 + 32 * g, v);
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * qe) << 16) + COL_D2 + 32 * g + 16 * eh, v);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&S.d2_empty[g]);
       {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = 16 * eh + jj;
           const int sj = __shfl_sync(0xffffffffu, myidx, j);
           if (j < nb && c < Cp) {
-            const float x = sj < 0 ? 0.f : v[j];
+            const float x = sj < 0 ? 0.f : v[jj];
             if (A.det) {
               const int64_t pos = start + b0 + j;
               A.dgc[(pos * 2 + half) * Cp + c] = x;
@@ -678,7 +680,7 @@ int launch_raster_bwd_tc(const gsparc_frame_layout& L, char* frame, int n_tx, in
     cudaFuncSetAttribute(k_raster_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC);
     attr_set = true;
   }
-  k_raster_bwd_tc<<<2 * L.ntiles, 256, SMEM_TC, st>>>(A);
+  k_raster_bwd_tc<<<2 * L.ntiles, 320, SMEM_TC, st>>>(A);
   return check_launch("k_raster_bwd_tc");
 }
 
