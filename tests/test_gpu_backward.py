@@ -128,14 +128,25 @@ def test_against_oracle(n, F, R, pose):
     assert max(err.values()) <= 1e-4, err
 
 
-def test_batched_backward_is_sum_of_singles(R, pose):
+@pytest.mark.parametrize("scene,B", [("perturbed", 4), ("perturbed", 8),
+                                     ("bwd_dup", 8), ("bwd_dup", 32)])
+def test_batched_backward_is_sum_of_singles(scene, B, R, pose):
+    """A batch of B TX (B*C columns: the tensor-core K5 from 16 columns) gives
+    the sum of the single-TX backward passes (2 columns: the CUDA-core K5),
+    including the reference's seam-duplicate rule (`bwd_dup`: a Gaussian
+    listed twice in a tile, only the later copy counts)."""
     import torch
     from paper_2511_22793_b200 import DeviceCloud
     from paper_2511_22793_b200.engine import split_flat
-    oc = O.round_f32(O.perturbed_scene(300, seed=4))
+    if scene == "bwd_dup":
+        fx = golden("bwd_dup")
+        oc = golden_cloud(fx)
+        assert (int(fx["w"]), int(fx["h"])) == (180, 45)
+    else:
+        oc = O.round_f32(O.perturbed_scene(300, seed=4))
     dc = DeviceCloud.from_host(host_cloud(oc))
-    txs = O.sample_tx(3, 4)
-    U = np.random.default_rng(6).normal(size=(4, 45, 180, 2))
+    txs = O.sample_tx(3, B)
+    U = np.random.default_rng(6).normal(size=(B, 45, 180, 2))
     _, frame = R.rasterize_forward_batch(dc, pose, txs, 180, 45,
                                          with_backward=True)
     dL = torch.as_tensor(U, dtype=torch.float32, device="cuda")
@@ -143,7 +154,7 @@ def test_batched_backward_is_sum_of_singles(R, pose):
     got = {k: v.double().cpu().numpy()
            for k, v in split_flat(flat, dc.n, dc.P).items()}
     want = {k: 0.0 for k in O.GROUPS}
-    for b in range(4):
+    for b in range(B):
         _, aux = R.rasterize_forward(dc, pose, txs[b], 180, 45)
         g = R.rasterize_backward(U[b], dc, pose, txs[b], aux).arrays()
         want = {k: want[k] + g[k] for k in O.GROUPS}
