@@ -278,59 +278,77 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
 //     L1 term + magnitude chain -> dL/dimg.
 // Same arithmetic (f64, taps in order) as the per-pixel kernels above, two
 // launches instead of six.
-constexpr int LB = 32;  // output columns per band
-
-// q = e / d for the small non-negative ranges of the band loops (e < 2^22)
-// without the ~20-instruction integer division: float estimate + fix-up
-struct FastDiv {
-  int d;
-  float inv;
-  __device__ FastDiv(int d_) : d(d_), inv(1.0f / (float)d_) {}
-  __device__ __forceinline__ int div(int e) const {
-    int q = __float2int_rz((float)e * inv);
-    const int r = e - q * d;
-    q += (r >= d) - (r < 0);
-    return q;
-  }
-};
+constexpr int LB = 32;        // output columns per band (the last band is padded)
+constexpr int XW = LB + 10;   // staged columns: the band + a 5-column halo each side
 
 __host__ __device__ inline int loss_nbands(int w) { return (w + LB - 1) / LB; }
 __host__ __device__ inline size_t loss_band_smem(int h) {
-  return sizeof(double) * (size_t)h * (size_t)(2 * (LB + 10) + 5 * LB);
+  return sizeof(double) * (size_t)h * (size_t)(2 * XW + 5 * LB);
 }
 __host__ __device__ inline size_t loss_adj_smem(int h) {
-  return sizeof(double) * (size_t)h * (size_t)(6 * (LB + 10));
+  return sizeof(double) * (size_t)h * (size_t)(6 * XW);
 }
 constexpr size_t LOSS_SMEM_MAX = 200 * 1024;
+
+// 11-tap window sum over a strided line with every tap in range
+__device__ __forceinline__ double tap11(const double (&wv)[11], const double* g, int stride) {
+  double acc = 0.0;
+#pragma unroll
+  for (int t = 0; t < 11; ++t) acc += wv[t] * g[t * stride];
+  return acc;
+}
+
+// out(i) = G(i) + [i < 5] G(-i-1) + [i >= n-5] G(2n-1-i), G(j) = sum_t w[t]
+// g[j+t-5] (g = 0 outside [0, n)); line element q at g[(q - q0) * stride]
+__device__ __forceinline__ double adj_fold(const double (&wv)[11], const double* g, int stride,
+                                          int q0, int n, int i) {
+  if (i >= 5 && i + 5 < n) return tap11(wv, g + (i - 5 - q0) * stride, stride);
+  auto G = [&](int j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+      const int q = j + t - 5;
+      if (q >= 0 && q < n) acc += wv[t] * g[(q - q0) * stride];
+    }
+    return acc;
+  };
+  double out = G(i);
+  if (i < 5) out += G(-i - 1);
+  if (i >= n - 5) out += G(2 * n - 1 - i);
+  return out;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   extern __shared__ double lsm[];
   const int h = A.h, w = A.w;
   const int p = blockIdx.y, b = p / A.S, s = p - b * A.S;
-  const int c0 = blockIdx.x * LB, wc = min(LB, w - c0), XW = wc + 10;
-  double* X = lsm;               // [h][XW]
-  double* Y = X + h * XW;        // [h][XW]
-  double* H5 = Y + h * XW;       // [5][h][wc]
-  // loads of several elements in flight per thread before the stores
-  const FastDiv dXW(XW), dWC(wc);
+  const int c0 = blockIdx.x * LB;
+  double wv[11];
+#pragma unroll
+  for (int t = 0; t < 11; ++t) wv[t] = A.win[t];
+  double* X = lsm;              // [h][XW]
+  double* Y = X + h * XW;       // [h][XW]
+  double* H5 = Y + h * XW;      // [5][h][LB]
+  // x / y with reflect-padded columns (columns past the image in a padded
+  // last band are staged too; their outputs are never written)
 #pragma unroll 4
   for (int e = threadIdx.x; e < h * XW; e += blockDim.x) {
-    const int r = dXW.div(e), cc = e - r * XW;
-    const int col = refl(c0 - 5 + cc, w);
+    const int r = e / XW, cc = e - r * XW;
+    const int col = refl(min(c0 - 5 + cc, 2 * w - 1), w);
     X[e] = pred_at(A, b, s, r, col);
     Y[e] = gt_at(A, b, s, r, col);
   }
   __syncthreads();
-  const int HW = h * wc;
+  const int HW = h * LB;
   for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = dWC.div(e), c = e - r * wc;
+    const int r = e / LB, c = e - r * LB;
     double a[5] = {0, 0, 0, 0, 0};
     const double* xr = X + r * XW + c;
     const double* yr = Y + r * XW + c;
 #pragma unroll
     for (int t = 0; t < 11; ++t) {
-      const double x = xr[t], y = yr[t], wt = A.win[t];
+      const double x = xr[t], y = yr[t], wt = wv[t];
       a[0] += wt * x;
       a[1] += wt * y;
       a[2] += wt * (x * x);
@@ -344,13 +362,23 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
   double v3[3] = {0.0, 0.0, 0.0};
   for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = dWC.div(e), c = e - r * wc;
+    const int r = e / LB, c = e - r * LB;
+    if (c0 + c >= w) continue;
     double m[5] = {0, 0, 0, 0, 0};
-    for (int t = 0; t < 11; ++t) {
-      const int rr = refl(r + t - 5, h);
-      const double wt = A.win[t];
+    if (r >= 5 && r + 5 < h) {  // interior rows: straight taps
+      const double* hc = H5 + (r - 5) * LB + c;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) m[k] += wt * H5[k * HW + rr * wc + c];
+      for (int t = 0; t < 11; ++t) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) m[k] += wv[t] * hc[k * HW + t * LB];
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const double* hc = H5 + refl(r + t - 5, h) * LB + c;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) m[k] += wv[t] * hc[k * HW];
+      }
     }
     const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
     const double mx = m[0], my = m[1];
@@ -388,67 +416,42 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   }
 }
 
-// G(j) = sum_t win[t] g[j + t - 5] over a line held in shared memory whose
-// element q of the image line sits at g[(q - q0) * stride], zero outside
-// [0, n); out(i) = G(i) + [i < 5] G(-i-1) + [i >= n-5] G(2n-1-i)
-template <typename T>
-__device__ __forceinline__ double adj_fold(const LossArgsT<T>& A, const double* g, int stride,
-                                          int q0, int n, int i) {
-  if (i >= 5 && i + 5 < n) {  // interior: all 11 taps in range, no fold-back
-    const double* gi = g + (i - 5 - q0) * stride;
-    double acc = 0.0;
-#pragma unroll
-    for (int t = 0; t < 11; ++t) acc += A.win[t] * gi[t * stride];
-    return acc;
-  }
-  auto G = [&](int j) {
-    double acc = 0.0;
-#pragma unroll
-    for (int t = 0; t < 11; ++t) {
-      const int q = j + t - 5;
-      if (q >= 0 && q < n) acc += A.win[t] * g[(q - q0) * stride];
-    }
-    return acc;
-  };
-  double out = G(i);
-  if (i < 5) out += G(-i - 1);
-  if (i >= n - 5) out += G(2 * n - 1 - i);
-  return out;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
   extern __shared__ double lsm[];
   const int h = A.h, w = A.w;
   const int p = blockIdx.y, b = p / A.S, s = p - b * A.S;
-  const int c0 = blockIdx.x * LB, wc = min(LB, w - c0), XW = wc + 10;
+  const int c0 = blockIdx.x * LB;
   const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
-  double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+wc+5
+  double wv[11];
+#pragma unroll
+  for (int t = 0; t < 11; ++t) wv[t] = A.win[t];
+  double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+LB+5
   double* Av = G + 3 * h * XW;     // [3][h][XW]
   const int HX = h * XW;
-  const FastDiv dHX(HX), dXW(XW), dWC(wc);
 #pragma unroll 4
   for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = dHX.div(e), rem = e - k * HX, r = dXW.div(rem), cc = rem - r * XW;
+    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
     const int col = c0 - 5 + cc;
     G[e] = (col >= 0 && col < w) ? A.G3[k * tot + (int64_t)p * plane + (int64_t)r * w + col] : 0.0;
   }
   __syncthreads();
   // adjoint along rows for every staged column (rows complete in smem)
   for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = dHX.div(e), rem = e - k * HX, r = dXW.div(rem), cc = rem - r * XW;
-    Av[e] = adj_fold(A, G + k * HX + cc, XW, 0, h, r);
+    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
+    Av[e] = adj_fold(wv, G + k * HX + cc, XW, 0, h, r);
   }
   __syncthreads();
   const double n = (double)plane;
   const double inv_n = 1.0 / n, k_l1 = (1.0 - A.lam) / (n * A.S), k_ss = A.lam / A.S;
-  for (int e = threadIdx.x; e < h * wc; e += blockDim.x) {
-    const int r = dWC.div(e), c = e - r * wc, col = c0 + c;
+  for (int e = threadIdx.x; e < h * LB; e += blockDim.x) {
+    const int r = e / LB, c = e - r * LB, col = c0 + c;
+    if (col >= w) continue;
     const double* row = Av + r * XW;
     // line index q = image column; element at (q - (c0 - 5))
-    const double amx = adj_fold(A, row, 1, c0 - 5, w, col);
-    const double ab2 = adj_fold(A, row + HX, 1, c0 - 5, w, col);
-    const double aa2 = adj_fold(A, row + 2 * HX, 1, c0 - 5, w, col);
+    const double amx = adj_fold(wv, row, 1, c0 - 5, w, col);
+    const double ab2 = adj_fold(wv, row + HX, 1, c0 - 5, w, col);
+    const double aa2 = adj_fold(wv, row + 2 * HX, 1, c0 - 5, w, col);
     const double x = pred_at(A, b, s, r, col), y = gt_at(A, b, s, r, col);
     const double gssim = (amx + 2 * x * ab2 + y * aa2) * inv_n;
     const double diff = x - y;
