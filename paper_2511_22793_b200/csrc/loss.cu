@@ -332,17 +332,24 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   double* H5 = Y + h * XW;      // [5][h][LB]
   // x / y with reflect-padded columns (columns past the image in a padded
   // last band are staged too; their outputs are never written)
+  // 2-D thread maps fixed per thread (no index divisions in the loops):
+  // staged rows of XW columns (24 rows per pass) and band rows of LB columns
+  // (32 rows per pass)
+  constexpr int RS = 1024 / XW;  // 24
+  const int sx = threadIdx.x % XW, sy = threadIdx.x / XW;
+  const int bx = threadIdx.x & (LB - 1), by = threadIdx.x >> 5;
+  if (sy < RS) {
+    const int col = refl(min(c0 - 5 + sx, 2 * w - 1), w);
 #pragma unroll 4
-  for (int e = threadIdx.x; e < h * XW; e += blockDim.x) {
-    const int r = e / XW, cc = e - r * XW;
-    const int col = refl(min(c0 - 5 + cc, 2 * w - 1), w);
-    X[e] = pred_at(A, b, s, r, col);
-    Y[e] = gt_at(A, b, s, r, col);
+    for (int r = sy; r < h; r += RS) {
+      X[r * XW + sx] = pred_at(A, b, s, r, col);
+      Y[r * XW + sx] = gt_at(A, b, s, r, col);
+    }
   }
   __syncthreads();
   const int HW = h * LB;
-  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = e / LB, c = e - r * LB;
+  for (int r = by; r < h; r += 32) {
+    const int c = bx, e = r * LB + c;
     double a[5] = {0, 0, 0, 0, 0};
     const double* xr = X + r * XW + c;
     const double* yr = Y + r * XW + c;
@@ -361,8 +368,8 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   __syncthreads();
   const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
   double v3[3] = {0.0, 0.0, 0.0};
-  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int r = e / LB, c = e - r * LB;
+  for (int r = by; r < h; r += 32) {
+    const int c = bx;
     if (c0 + c >= w) continue;
     double m[5] = {0, 0, 0, 0, 0};
     if (r >= 5 && r + 5 < h) {  // interior rows: straight taps
@@ -429,23 +436,32 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
   double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+LB+5
   double* Av = G + 3 * h * XW;     // [3][h][XW]
   const int HX = h * XW;
+  constexpr int RS = 1024 / XW;  // 24 staged rows per pass
+  const int sx = threadIdx.x % XW, sy = threadIdx.x / XW;
+  const int bx = threadIdx.x & (LB - 1), by = threadIdx.x >> 5;
+  if (sy < RS) {
+    const int col = c0 - 5 + sx;
+    const bool in = col >= 0 && col < w;
+    const double* g3 = A.G3 + (int64_t)p * plane + col;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
 #pragma unroll 4
-  for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
-    const int col = c0 - 5 + cc;
-    G[e] = (col >= 0 && col < w) ? A.G3[k * tot + (int64_t)p * plane + (int64_t)r * w + col] : 0.0;
+      for (int r = sy; r < h; r += RS)
+        G[k * HX + r * XW + sx] = in ? g3[k * tot + (int64_t)r * w] : 0.0;
   }
   __syncthreads();
   // adjoint along rows for every staged column (rows complete in smem)
-  for (int e = threadIdx.x; e < 3 * HX; e += blockDim.x) {
-    const int k = e / HX, rem = e - k * HX, r = rem / XW, cc = rem - r * XW;
-    Av[e] = adj_fold(wv, G + k * HX + cc, XW, 0, h, r);
+  if (sy < RS) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      for (int r = sy; r < h; r += RS)
+        Av[k * HX + r * XW + sx] = adj_fold(wv, G + k * HX + sx, XW, 0, h, r);
   }
   __syncthreads();
   const double n = (double)plane;
   const double inv_n = 1.0 / n, k_l1 = (1.0 - A.lam) / (n * A.S), k_ss = A.lam / A.S;
-  for (int e = threadIdx.x; e < h * LB; e += blockDim.x) {
-    const int r = e / LB, c = e - r * LB, col = c0 + c;
+  for (int r = by; r < h; r += 32) {
+    const int c = bx, col = c0 + c;
     if (col >= w) continue;
     const double* row = Av + r * XW;
     // line index q = image column; element at (q - (c0 - 5))
