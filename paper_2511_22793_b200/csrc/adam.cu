@@ -77,9 +77,9 @@ __device__ __forceinline__ double adam_upd(double g, float& m, float& v, double 
   return lr * (mm / bc1) / (sqrt(vv / bc2) + eps);
 }
 
-// Blocks [0, geo_blocks): thread per Gaussian -- positions, log-scales,
-// rotations (renormalised right after their update, scene.py:117-122) and
-// the opacity; the remaining blocks: the MLP weights, 4 per thread.
+// Blocks [0, geo_blocks): the geometry (f64): a thread per position,
+// log-scale and opacity element, a thread per Gaussian's rotation; the
+// remaining blocks: the MLP weights, 4 per thread.
 __global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
   // a frame whose pair buffer overflowed produced no valid gradient
   if (A.counters[GSPARC_CNT_NONFINITE] || A.counters[GSPARC_CNT_OVERFLOW]) return;
@@ -97,34 +97,34 @@ __global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
   const double bc1 = s_sc[0], bc2 = s_sc[1];
   const int64_t n = A.n;
   if ((int)blockIdx.x < geo_blocks) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    for (int k = 0; k < 3; ++k) {
-      const int64_t e = 3 * i + k;
-      A.pos[e] -= adam_upd((double)A.g[e], A.m[e], A.v[e], s_sc[2], b1, b2, bc1, bc2, eps);
-    }
-    for (int k = 0; k < 3; ++k) {
-      const int64_t e = 3 * n + 3 * i + k;
-      A.ls[3 * i + k] -=
-          adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.scaling_lr, b1, b2, bc1, bc2, eps);
-    }
-    double q[4];
-    for (int k = 0; k < 4; ++k) {
-      const int64_t e = 6 * n + 4 * i + k;
-      q[k] = A.rot[4 * i + k] -
-             adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.rotation_lr, b1, b2, bc1, bc2, eps);
-    }
-    // normalize_quaternions (scene.py:117-122)
-    const double nr = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-    if (nr > 0.0) {
-      for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k] / nr;
-    } else {
-      for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k];
-      atomicOr(A.counters + GSPARC_CNT_NONFINITE, 1 << 5);
-    }
-    {
-      const int64_t e = 10 * n + i;
+    // geometry, f64: thread per position / log-scale / opacity element
+    // (t < 7n), thread per Gaussian for the rotations (renormalised right
+    // after their update, scene.py:117-122)
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 3 * n) {
+      A.pos[t] -= adam_upd((double)A.g[t], A.m[t], A.v[t], s_sc[2], b1, b2, bc1, bc2, eps);
+    } else if (t < 6 * n) {
+      A.ls[t - 3 * n] -=
+          adam_upd((double)A.g[t], A.m[t], A.v[t], A.cfg.scaling_lr, b1, b2, bc1, bc2, eps);
+    } else if (t < 7 * n) {
+      const int64_t i = t - 6 * n, e = 10 * n + i;
       A.op[i] -= adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.opacity_lr, b1, b2, bc1, bc2, eps);
+    } else if (t < 8 * n) {
+      const int64_t i = t - 7 * n;
+      double q[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t e = 6 * n + 4 * i + k;
+        q[k] = A.rot[4 * i + k] -
+               adam_upd((double)A.g[e], A.m[e], A.v[e], A.cfg.rotation_lr, b1, b2, bc1, bc2, eps);
+      }
+      const double nr = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+      if (nr > 0.0) {
+        for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k] / nr;
+      } else {
+        for (int k = 0; k < 4; ++k) A.rot[4 * i + k] = q[k];
+        atomicOr(A.counters + GSPARC_CNT_NONFINITE, 1 << 5);
+      }
     }
     return;
   }
@@ -138,13 +138,27 @@ __global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
   // all loads of the 4 elements first, then 4 independent f64 chains
   const int kn = (int)min((int64_t)4, cnt - 4 * q);
   float gv[4], mv[4], vv[4], wv[4];
+  // 16-byte vectors when the MLP block of the flat buffer is aligned
+  // (11 n % 4 == 0) and all four elements exist
+  const bool vec = ((base & 3) == 0) && kn == 4;
+  if (vec) {
+    const float4 g4 = *reinterpret_cast<const float4*>(A.g + e0);
+    const float4 m4 = *reinterpret_cast<const float4*>(A.m + e0);
+    const float4 v4 = *reinterpret_cast<const float4*>(A.v + e0);
+    const float4 w4 = *reinterpret_cast<const float4*>(A.mlp + (e0 - base));
+    gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
+    mv[0] = m4.x; mv[1] = m4.y; mv[2] = m4.z; mv[3] = m4.w;
+    vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+    wv[0] = w4.x; wv[1] = w4.y; wv[2] = w4.z; wv[3] = w4.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k < kn) {
-      gv[k] = A.g[e0 + k];
-      mv[k] = A.m[e0 + k];
-      vv[k] = A.v[e0 + k];
-      wv[k] = A.mlp[e0 + k - base];
+    for (int k = 0; k < 4; ++k) {
+      if (k < kn) {
+        gv[k] = A.g[e0 + k];
+        mv[k] = A.m[e0 + k];
+        vv[k] = A.v[e0 + k];
+        wv[k] = A.mlp[e0 + k - base];
+      }
     }
   }
   // f32 moments and update for the f32 weights (the stored m, v are f32;
@@ -163,12 +177,18 @@ __global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
       wv[k] -= lrf * (mm * ib1) / (sqrtf(v2 * ib2) + epsf);
     }
   }
+  if (vec) {
+    *reinterpret_cast<float4*>(A.m + e0) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+    *reinterpret_cast<float4*>(A.v + e0) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    *reinterpret_cast<float4*>(A.mlp + (e0 - base)) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+  } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k < kn) {
-      A.m[e0 + k] = mv[k];
-      A.v[e0 + k] = vv[k];
-      A.mlp[e0 + k - base] = wv[k];
+    for (int k = 0; k < 4; ++k) {
+      if (k < kn) {
+        A.m[e0 + k] = mv[k];
+        A.v[e0 + k] = vv[k];
+        A.mlp[e0 + k - base] = wv[k];
+      }
     }
   }
 }
@@ -189,7 +209,7 @@ int launch_adam(double* pos, double* ls, double* rot, double* op, float* mlp, in
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   k_check_finite<<<blocks, 256, 0, st>>>(A, total);
-  const int geo_blocks = (int)((n + 255) / 256);
+  const int geo_blocks = (int)((8 * n + 255) / 256);
   const int64_t mlp4 = (n * (int64_t)P + 3) / 4;
   const int mlp_blocks = (int)((mlp4 + 255) / 256);
   if (geo_blocks + mlp_blocks > 0) k_adam<<<geo_blocks + mlp_blocks, 256, 0, st>>>(A, total, geo_blocks);
