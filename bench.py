@@ -988,10 +988,16 @@ def run_train(args):
                 for _ in range(2)]
     stats_host = [torch.empty((Bl, _lib.LOSS_STATS), dtype=torch.float64).pin_memory()
                   for _ in range(2)]
-    staged = [torch.cuda.Event() for _ in range(2)]
+    # two device slots in the dataset buffers (samples [0, Bl) and [Bl, 2Bl)
+    # are overwritten by the streamed batches): the H2D of step i+1 runs on
+    # a copy stream while step i computes
+    slot_idx = [torch.arange(k * Bl, (k + 1) * Bl, device="cuda") for k in range(2)]
+    copy_stream = torch.cuda.Stream()
+    copied = [torch.cuda.Event() for _ in range(2)]   # slot k filled (copy stream)
+    used = [torch.cuda.Event() for _ in range(2)]     # slot k consumed (compute stream)
     for k in range(2):
-        staged[k].record(stream)
-    tr.idx.copy_(torch.arange(Bl, device="cuda"))
+        used[k].record(stream)
+        copied[k].record(copy_stream)
     from paper_2511_22793_b200 import dp
 
     def e2e_run(nsteps):
@@ -999,14 +1005,19 @@ def run_train(args):
             k = i & 1
             local_ids = dp.shard(np.asarray(batches[i % len(batches)]), tr.rank,
                                  tr.world)
-            staged[k].synchronize()                 # staging buffer k free
+            copied[k].synchronize()               # pinned stage k free again
             ids = torch.as_tensor(local_ids)
             torch.index_select(gt_host, 0, ids, out=stage_gt[k])
             torch.index_select(tx_host, 0, ids, out=stage_tx[k])
-            tr.gt_all[:Bl].copy_(stage_gt[k], non_blocking=True)
-            tr.tx_all[:Bl].copy_(stage_tx[k], non_blocking=True)
-            staged[k].record(stream)
+            copy_stream.wait_event(used[k])       # the step reading slot k is done
+            with torch.cuda.stream(copy_stream):
+                tr.gt_all[k * Bl:(k + 1) * Bl].copy_(stage_gt[k], non_blocking=True)
+                tr.tx_all[k * Bl:(k + 1) * Bl].copy_(stage_tx[k], non_blocking=True)
+                copied[k].record(copy_stream)
+            stream.wait_event(copied[k])
+            tr.idx.copy_(slot_idx[k])
             st = tr.step(None)
+            used[k].record(stream)
             stats_host[k].copy_(st.to(torch.float64), non_blocking=True)
 
     e2e_steps = min(args.steps, 50)
@@ -1073,8 +1084,10 @@ def run_train(args):
                         "d2h_bytes_per_step": Bl * 8 * _lib.LOSS_STATS,
                         "path": "per step: the rank's batch of TX + ground "
                                 "truth gathered on the host into pinned "
-                                "memory, copied H2D, Trainer.step (graph + "
-                                "all-reduce + Adam), loss stats copied D2H"}}
+                                "memory, copied H2D on a copy stream into one "
+                                "of two device slots (overlapping the previous "
+                                "step), Trainer.step (graph + all-reduce + "
+                                "Adam), loss stats copied D2H"}}
         if world == 1 and not args.no_cpu_baseline:
             gtn = gt[:3].double().cpu().numpy()
             line["cpu_baseline"] = cpu_baseline_train(cloud, txs[:3], gtn, w,
