@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
 }
 
 bool raster_bwd_tc_supported(const gsparc_frame_layout& L, int64_t Cp) {
-  return L.dtype == GSPARC_F32 && Cp >= 16 && Cp <= TC_KMAX;
+  // the loader reads coef rows as float2 pairs: even row lengths only
+  return L.dtype == GSPARC_F32 && Cp >= 16 && Cp <= TC_KMAX && (Cp & 1) == 0;
 }
 
 int launch_raster_bwd_tc(const gsparc_frame_layout& L, char* frame, int n_tx, int C,
