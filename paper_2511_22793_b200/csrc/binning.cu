@@ -225,7 +225,8 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
 // (coarse32, index) and written back to a in sorted order.  Ends with the
 // CTA's writes to a visible to the CTA.
 __device__ void bucket_pass(uint64_t* a, uint64_t* b, int* bcnt, int* bcur, int n,
-                            uint32_t cmin, int bshift) {
+                            uint32_t cmin, int bshift, long long* dbg = nullptr,
+                            long long t_dbg0 = 0) {
   // exclusive scan of the bucket counts (BK_N / blockDim per thread)
   constexpr int PER = BK_N / RS_T;
   int loc[PER];
@@ -269,6 +270,7 @@ __device__ void bucket_pass(uint64_t* a, uint64_t* b, int* bcnt, int* bcur, int 
     b[atomicAdd(bcur + bk, 1)] = v;
   }
   __syncthreads();
+  if (dbg && threadIdx.x == 0) *dbg = clock64() - t_dbg0;
   // every key's rank inside its bucket: one pass over the (small)
   // bucket per key, all keys in parallel; written to a in sorted order
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -294,78 +296,110 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   // launched as a dependent of K2: every histogram and segment is written
   // once K2's grid has completed
   pdl_wait();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 0] = clock64() - t_dbg0;
   extern __shared__ uint64_t s_keys[];  // 2 * RS_CAP keys + counters
-  __shared__ int s_start[2];
-  __shared__ int s_pos;
+  __shared__ int s_pos, s_ovf;
+  __shared__ int s_w[2][RS_W];
   __shared__ uint32_t s_mm[2];
-  const int t = blockIdx.x;
-  int* sc = (int*)(s_keys + 2 * RS_CAP);  // tile scan [ntiles + 1] + tmp [RS_W + 1]
-  int* s_soff = sc + A.ntiles + RS_W + 2;  // staged segments: offset, length, prefix
-  int* s_slen = s_soff + SEG_MAX;
-  int* s_spre = s_slen + SEG_MAX;
-  // the segment descriptors are loaded first so their latency overlaps the
-  // tile scan
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned full = 0xffffffffu;
+  // every global read of the prologue is issued before the first wait: the
+  // overflow flag, this tile's count and the counts before it (its list
+  // offset), and the staged-segment descriptors.  Warp w takes segments
+  // [w S, w S + S), S = ceil(nseg / 32): lane l holds segment w S + 32 k + l.
   const int nseg = (int)A.seg_stride;  // one slot per preprocess CTA (length 0: empty)
   const int2* sg = A.seg + (int64_t)t * A.seg_stride;
   const bool seg_fast = nseg <= SEG_MAX;
-  int2 dsc[SEG_MAX / RS_T];
-  if (seg_fast) {
-#pragma unroll
-    for (int k = 0; k < SEG_MAX / RS_T; ++k) {
-      const int j = threadIdx.x + k * RS_T;
-      dsc[k] = j < nseg ? __ldcg(sg + j) : make_int2(0, 0);
-    }
-  }
-  // tile_start = exclusive scan of the per-tile pair counts
-  block_exclusive_scan(A.tile_count, sc, A.ntiles, sc + A.ntiles + 1);
-  if (t == 0)
-    for (int j = threadIdx.x; j <= A.ntiles; j += blockDim.x) A.tile_start[j] = sc[j];
-  if (threadIdx.x == 0) {
-    s_start[0] = sc[t];
-    s_start[1] = sc[t + 1];
+  const int S = (nseg + 31) >> 5;
+  if (tid == 0) {
+    s_ovf = __ldcg(A.counters + GSPARC_CNT_OVERFLOW);
     s_pos = 0;
     s_mm[0] = 0xFFFFFFFFu;
     s_mm[1] = 0u;
   }
-  if (seg_fast) {
+  const int n = __ldcg(A.tile_count + t);
+  int pre_t = 0;
+  for (int i = tid; i < t; i += RS_T) pre_t += __ldcg(A.tile_count + i);
+  int2 d[SEG_MAX / RS_T];
 #pragma unroll
-    for (int k = 0; k < SEG_MAX / RS_T; ++k) {
-      const int j = threadIdx.x + k * RS_T;
-      if (j < nseg) {
-        s_soff[j] = dsc[k].x;
-        s_slen[j] = dsc[k].y;
-      }
+  for (int k = 0; k < SEG_MAX / RS_T; ++k) {
+    const int r = 32 * k + lane, j = warp * S + r;
+    d[k] = seg_fast && r < S && j < nseg ? __ldcg(sg + j) : make_int2(0, 0);
+  }
+  // segment positions inside the tile's list: scan in (warp, k, lane) order
+  int rowpre[SEG_MAX / RS_T];
+  int wtot = 0;
+#pragma unroll
+  for (int k = 0; k < SEG_MAX / RS_T; ++k) {
+    int inc = d[k].y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(full, inc, o);
+      if (lane >= o) inc += u;
     }
+    rowpre[k] = wtot + inc - d[k].y;
+    wtot += __shfl_sync(full, inc, 31);
+  }
+  pre_t = __reduce_add_sync(full, pre_t);
+  if (lane == 0) {
+    s_w[0][warp] = wtot;
+    s_w[1][warp] = pre_t;
   }
   __syncthreads();
-  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 1] = clock64() - t_dbg0;
-  if (A.counters[GSPARC_CNT_OVERFLOW]) {
+  const int s = __reduce_add_sync(full, s_w[1][lane]);  // tile_start[t]
+  int wbase = s_w[0][lane];
+  {
+    int inc = wbase;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(full, inc, o);
+      if (lane >= o) inc += u;
+    }
+    wbase = __shfl_sync(full, inc - wbase, warp);
+  }
+  if (A.dbg && tid == 0) A.dbg[blockIdx.x * 16 + 1] = clock64() - t_dbg0;
+  if (s_ovf) {
     // the staged pairs are incomplete: no list, but the tile is still
     // published so that pass-A CTAs waiting on the queue see the overflow
     // (K2 has completed, so the flag is final) and exit
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
+      A.tile_start[t] = s;
+      A.tile_start[t + 1] = s + n;
+      __threadfence();
       const int q = atomicAdd(A.counters + GSPARC_CNT_SORTED, 1);
       flag_release(A.ready + q, t + 1);
     }
     return;
   }
-  const int s = s_start[0], n = s_start[1] - s;
   uint64_t* g = A.pairs + s;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
   if (seg_fast && n <= RS_CAP) {
+    // segment table in shared memory (the bucket counters' space, unused
+    // until the histogram): offset, length, list position
+    int* s_soff = (int*)(s_keys + 2 * RS_CAP);
+    int* s_slen = s_soff + SEG_MAX;
+    int* s_spre = s_slen + SEG_MAX;
+    const int mybase = wbase;
+#pragma unroll
+    for (int k = 0; k < SEG_MAX / RS_T; ++k) {
+      const int r = 32 * k + lane, j = warp * S + r;
+      if (r < S && j < nseg) {
+        s_soff[j] = d[k].x;
+        s_slen[j] = d[k].y;
+        s_spre[j] = mybase + rowpre[k];
+      }
+    }
+    __syncthreads();
     // thread t gathers keys [t*per, t*per + per): one binary search over the
-    // segment prefix for its first key, then it walks forward through the
+    // segment positions for its first key, then it walks forward through the
     // (on average longer than per) segments; all its loads are in flight
     // together
-    block_exclusive_scan(s_slen, s_spre, nseg, sc + A.ntiles + 1);
-    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 8] = clock64() - t_dbg0;
     const int per = (n + RS_T - 1) / RS_T;  // <= RS_E
-    const int j0 = threadIdx.x * per;
+    const int j0 = tid * per;
     uint64_t v[RS_E];
     if (j0 < n) {
-      int l = 0;  // last segment with prefix <= j0
-#pragma unroll
-      for (int step = SEG_MAX / 2; step >= 1; step >>= 1)
+      int l = 0;  // last segment with position <= j0
+      for (int step = 1 << (31 - __clz(nseg)); step >= 1; step >>= 1)
         if (l + step < nseg && s_spre[l + step] <= j0) l += step;
       int sbeg = s_spre[l], send = sbeg + s_slen[l], soff = s_soff[l];
 #pragma unroll
@@ -382,9 +416,6 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
           v[e] = __ldcg(A.stage + soff + (j - sbeg));
         }
       }
-    }
-    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_dbg0;
-    if (j0 < n) {
 #pragma unroll
       for (int e = 0; e < RS_E; ++e) {
         const int j = j0 + e;
@@ -396,13 +427,14 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
         }
       }
     }
+    if (A.dbg && tid == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_dbg0;
   } else {  // one thread per staged segment (any order, the sort is total)
     uint64_t* dst = n <= RS_CAP ? s_keys : g;
-    for (int j = threadIdx.x; j < nseg; j += blockDim.x) {
-      const int2 d = __ldcg(sg + j);
-      const int p = atomicAdd(&s_pos, d.y);
-      const uint64_t* src = A.stage + d.x;
-      for (int k = 0; k < d.y; ++k) {
+    for (int j = tid; j < nseg; j += blockDim.x) {
+      const int2 dj = __ldcg(sg + j);
+      const int p = atomicAdd(&s_pos, dj.y);
+      const uint64_t* src = A.stage + dj.x;
+      for (int k = 0; k < dj.y; ++k) {
         const uint64_t x = __ldcg(src + k);
         dst[p + k] = x;
         const uint32_t c = (uint32_t)(x >> 32);
@@ -445,7 +477,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
     if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 3] = clock64() - t_dbg0;
     uint64_t* r;
     if (s_bmax < BK_BIG) {
-      bucket_pass(a, b, bcnt, bcur, n, cmin, bshift);
+      bucket_pass(a, b, bcnt, bcur, n, cmin, bshift, A.dbg ? A.dbg + blockIdx.x * 16 + 4 : nullptr, t_dbg0);
       __syncthreads();
       if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 5] = clock64() - t_dbg0;
       r = a;
@@ -539,12 +571,10 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st,
   A.dbg = nullptr;
   if (experiment_env("GSPARC_SORT_DBG")) A.dbg = dbg_rows(0);  // experiments only
   const size_t cnt_ints =
-      (size_t)max(max(RS_W * 256 + 512, 2 * BK_N), L.ntiles + RS_W + 2 + 3 * SEG_MAX + 1);
+      (size_t)max(RS_W * 256 + 512, 2 * BK_N);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;
-  if (smem_sort > 227 * 1024) {
-    set_error("bin_tiles: %d tiles exceed the sort kernel's shared memory", L.ntiles);
-    return GSPARC_ERR_UNSUPPORTED;
-  }
+  static_assert(2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * 2 * BK_N <= 227 * 1024,
+                "k_tile_sort shared memory");
   static size_t attr_set = 0;
   if (attr_set < smem_sort) {
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sort);

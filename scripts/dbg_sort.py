@@ -17,10 +17,23 @@ L = _lib.lib()
 n = 138
 host = (ctypes.c_longlong * (12288 * 16))()
 assert L.gsparc_debug_copy(host, ctypes.c_int64(12288 * 16)) == 0
-d = np.ctypeslib.as_array(host).reshape(12288, 16)[0 * 4096:0 * 4096 + n][:, :10]
+d = np.ctypeslib.as_array(host).reshape(12288, 16)[0 * 4096:0 * 4096 + n][:, :11]
 ts = frame.view("tile_start", torch.int32, (n + 1,)).cpu().numpy()
 ln = np.diff(ts)
-print("phase ends: prologue gather hist scan+scatter rank - ties+write | seg-scan search+load-issue")
-print("avg", d.mean(0).astype(int))
-for r in np.argsort(-d[:, 7])[:6]:
-    print("tile", r, "n", ln[r], d[r].astype(int))
+# cycle stamps since kernel start: 0 pdl_wait done, 1 prologue (descriptor
+# and count loads, segment scan), 9 segment copies, 2 min/max, 3 histogram,
+# 4 bucket scatter, 5 bucket rank, 7 ties
+cols = [0, 1, 9, 2, 3, 4, 5, 7]
+names = ["wait", "prolog", "copy", "minmax", "hist", "scatter", "rank", "ties"]
+def row(v):
+    st = v[cols].astype(int)
+    return " ".join("%s=%d" % (nm, st[k] - (st[k - 1] if k else 0)) for k, nm in enumerate(names)) + " total_after_wait=%d" % (st[-1] - st[0])
+print("per-phase cycles (differences of consecutive stamps)")
+print("avg       ", row(d.mean(0)))
+small = ln < 2000
+print("avg n<2000", row(d[small].mean(0)), "tiles", small.sum())
+print("avg n>=2000", row(d[~small].mean(0)))
+for r in np.argsort(-d[:, 7])[:4]:
+    print("tile", r, "n", ln[r], row(d[r]))
+for r in np.where(small)[0][:4]:
+    print("tile", r, "n", ln[r], row(d[r]))
