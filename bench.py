@@ -696,6 +696,8 @@ def run_ours(args):
                                           "44N + 4 N_live P + B(12 + 4HWC)"},
             "live_fraction": (live / kept) if (live is not None and kept) else None,
             "pairs": pairs, "stages_us": stages,
+            "stage_traffic": stage_traffic(stages, n, P, C, B, h, w, live, pairs,
+                                           args.config),
         }
         if cpu_line is not None:
             line["cpu_baseline"] = cpu_line
@@ -817,11 +819,11 @@ def ncu_kernel_stats(config, stage):
         return None
 
 
-def roofline_entry(dom, stages, n, P, C, B, h, w, live, pairs, hbm, config):
-    """Algorithmic bytes of the dominant stage / its measured duration."""
-    us = stages[dom]
+def stage_bytes(n, P, C, B, h, w, live, pairs):
+    """Algorithmic HBM bytes per launch of each render stage (DESIGN.md
+    section 3's per-unit figures times the units of one launch)."""
     nl = live if live is not None else n
-    per = {
+    return {
         # geometry read (f64 pos/scale/quat/logit = 88 B) + records written
         # (key 8 + rec32 32 + rect 16)
         "preprocess": n * (88 + 56),
@@ -834,12 +836,45 @@ def roofline_entry(dom, stages, n, P, C, B, h, w, live, pairs, hbm, config):
         "mlp": n * 4 * (P + B * C),
         "raster_accumulate": pairs * 8 + nl * 4 * B * C + 4 * h * w * B * C,
         "raster_fused": pairs * 8 + n * 4 * B * C + 4 * h * w * B * C + h * w * 12,
-    }[dom]
+    }
+
+
+def pipe_traffic(config):
+    """In-pipeline DRAM bytes per stage (profiles/ncu_pipe_traffic.json,
+    scripts/gpu_traffic_pipe.sh: ncu --cache-control none, so each kernel
+    sees the L2 its predecessor left, as in the graph); {} if not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_pipe_traffic.json")) as f:
+            return json.load(f)["configs"][config]
+    except (OSError, ValueError, KeyError):
+        return {}
+
+
+def stage_traffic(stages, n, P, C, B, h, w, live, pairs, config):
+    """Per stage: algorithmic bytes, measured in-pipeline DRAM bytes and
+    their ratio (traffic well above the algorithmic bytes = wasted re-reads)."""
+    per = stage_bytes(n, P, C, B, h, w, live, pairs)
+    pt = pipe_traffic(config)
+    out = {}
+    for st in stages:
+        if st not in per:
+            continue
+        d = pt.get(st, {}).get("dram_bytes")
+        out[st] = {"algorithmic_bytes": per[st], "dram_bytes_in_pipeline": d,
+                   "ratio": d / per[st] if d else None}
+    return out
+
+
+def roofline_entry(dom, stages, n, P, C, B, h, w, live, pairs, hbm, config):
+    """Algorithmic bytes of the dominant stage / its measured duration."""
+    us = stages[dom]
+    per = stage_bytes(n, P, C, B, h, w, live, pairs)[dom]
     achieved = per / (us * 1e-6) / 1e9
     nc = ncu_kernel_stats(config, dom)
     out = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
            "unit": "GB/s", "frac": achieved / hbm,
            "traffic": nc.get("dram_bytes") if nc else None,
+           "traffic_in_pipeline": pipe_traffic(config).get(dom, {}).get("dram_bytes"),
            "algorithmic_bytes": per, "launch_us": us,
            "note": "raster stages are issue/latency-bound (alpha compositing "
                    "on CUDA cores, sequential transmittance), so their HBM "

@@ -63,6 +63,7 @@ struct PxArgs {
   const int* ready;  // pass A: K3's per-tile flags (null: the sort grid has completed)
   int pdl_b;         // pass B launched as a dependent (upstream reads after the wait)
   int mix_b;         // pass B: interleave top/bottom tiles in launch order
+  int tile_major_b;  // pass B, several channel chunks: a half tile's chunk CTAs adjacent
   int wmax;
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
@@ -549,16 +550,24 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   // (tile, half) of this CTA: with mix_b, consecutive CTAs alternate between
   // a tile of the top half of the image and one of the bottom half, so the
   // two CTAs an SM receives together rarely are both of a heavy tile row
-  int cta = blockIdx.x;
+  int cta = blockIdx.x, ychunk = blockIdx.y;
   if (A.mix_b) {
     const int k = blockIdx.x >> 1, nt = A.ntiles;
     const int tile = (k & 1) ? nt - 1 - (k >> 1) : (k >> 1);
     cta = 2 * tile + (blockIdx.x & 1);
   }
+  if (A.tile_major_b) {
+    // the channel-chunk CTAs of one half tile are consecutive in launch
+    // order, so they run together: its stored weights come from DRAM once
+    // (then L2) and its pixels' image rows are completed while in L2
+    const int lin = blockIdx.x + blockIdx.y * gridDim.x;
+    cta = lin / gridDim.y;
+    ychunk = lin - cta * gridDim.y;
+  }
   if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 12] = gtimer();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CtaGeom g = cta_geom(A, cta);
-  const int col0 = blockIdx.y * NP;
+  const int col0 = ychunk * NP;
   // ordinary launch: the chunk count and list bounds are read first so their
   // latency overlaps the prologue; a dependent launch reads them after its
   // grid-dependency wait
@@ -935,6 +944,8 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   // or behind pass A (config 1) it was 1-2% slower, so it is off there
   static const int mix = experiment_env("GSPARC_PXB_MIX") ? atoi(experiment_env("GSPARC_PXB_MIX")) : -1;
   B.mix_b = mix >= 0 ? mix : (after_mlp && chunks_y == 1);
+  static const int tmaj = experiment_env("GSPARC_PXB_TMAJ") ? atoi(experiment_env("GSPARC_PXB_TMAJ")) : 1;
+  B.tile_major_b = chunks_y > 1 && tmaj && !B.mix_b;
   if (experiment_env("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   // dependent launch behind the streaming MLP (render path, pass 2): the
   // prologue (TMEM allocation, barriers, stage clearing) overlaps the MLP's
@@ -988,6 +999,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.ready = nullptr;
   A.pdl_b = 0;
   A.mix_b = 0;
+  A.tile_major_b = 0;
   A.Cp = (int64_t)n_tx * C;
   A.n = L.n;
   A.C = C;
