@@ -39,6 +39,7 @@ struct SortArgs {
   int ntx;
   int ntiles;
   long long* dbg;  // experiments: per-CTA phase clocks (GSPARC_SORT_DBG)
+  int long_bits;   // bucket bits of the long-list path
 };
 
 // Ascending-only bitonic network on n elements (virtual +inf padding up to
@@ -219,6 +220,40 @@ __device__ uint64_t* block_radix_sort(uint64_t* src, uint64_t* dst, int* cnt, in
   return src;  // buffer holding the result
 }
 
+// In-place exclusive scan of c[0 .. PER * RS_T) (PER consecutive counts per
+// thread); c[PER * RS_T] = total.  Ends with a barrier.
+template <int PER>
+__device__ void scan_counts(int* c) {
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) sum += c[threadIdx.x * PER + k];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  __shared__ int s_ws[RS_W];
+  if (lane == 31) s_ws[wid] = inc;
+  __syncthreads();
+  int x = s_ws[lane];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
+  }
+  int run = inc - sum + __shfl_sync(0xffffffffu, x - s_ws[lane], wid);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int v = c[threadIdx.x * PER + k];
+    c[threadIdx.x * PER + k] = run;
+    run += v;
+  }
+  if (threadIdx.x == RS_T - 1) c[PER * RS_T] = run;
+  __syncthreads();
+}
+
 // One bucket pass of K3 on keys a[0..n) (shared or global memory): bcnt holds
 // the BK_N bucket counts on entry; exclusive scan -> bucket starts, scatter
 // a -> b by bucket, then every key is ranked inside its (small) bucket by
@@ -285,6 +320,108 @@ __device__ void bucket_pass(uint64_t* a, uint64_t* b, int* bcnt, int* bcur, int 
     a[rank] = v;
   }
   __syncthreads();
+}
+
+// K3 for lists longer than shared memory: one bucket pass on the top GB bits
+// of the tile-relative coarse key with the keys in L2 (the list g and a
+// scratch slice tmp of the same offsets) and 2^GB bucket cursors in shared
+// memory, then whole-bucket windows of <= WCAP keys ranked in shared memory;
+// a bucket of >= BK_BIG_G keys falls back to a bitonic sort.
+template <int GB>
+__device__ void sort_long_list(const SortArgs& A, uint64_t* s_keys, uint64_t* g, int n, int s,
+                               uint32_t cmin, uint32_t cmax, long long t_dbg0) {
+  constexpr int GN = 1 << GB, WCAP = GB > BK_BITS + 1 ? RS_CAP / 2 : RS_CAP;
+  uint64_t* wa = s_keys;
+  uint64_t* wb = s_keys + WCAP;
+  int* cur = (int*)(s_keys + 2 * WCAP);  // [GN + 1]: counts, then starts, then ends
+  const uint32_t span = cmax - cmin;
+  const int bits = span ? 32 - __clz(span) : 0;
+  const int bshift = bits > GB ? bits - GB : 0;
+  __shared__ int s_gbig;
+  if (threadIdx.x == 0) s_gbig = 0;
+  for (int q = threadIdx.x; q < GN; q += blockDim.x) cur[q] = 0;
+  __syncthreads();
+  // RS_E keys' loads in flight per thread, then their counter atomics
+  for (int j0 = threadIdx.x; j0 < n; j0 += RS_CAP) {
+    uint64_t v[RS_E];
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int j = j0 + e * RS_T;
+      v[e] = j < n ? __ldcg(g + j) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      if (j0 + e * RS_T < n) {
+        const int bk = (int)(((uint32_t)(v[e] >> 32) - cmin) >> bshift);
+        if (atomicAdd(cur + bk, 1) == BK_BIG_G) s_gbig = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 3] = clock64() - t_dbg0;
+  if (s_gbig || !A.sort_tmp) {
+    bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
+    __syncthreads();
+    fix_coarse_ties(g, n, A.key);
+    __syncthreads();
+    return;
+  }
+  uint64_t* tmp = A.sort_tmp + s;
+  scan_counts<GN / RS_T>(cur);  // cur = bucket starts
+  for (int j0 = threadIdx.x; j0 < n; j0 += RS_CAP) {  // scatter by bucket
+    uint64_t v[RS_E];
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      const int j = j0 + e * RS_T;
+      v[e] = j < n ? __ldcg(g + j) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < RS_E; ++e) {
+      if (j0 + e * RS_T < n) {
+        const int bk = (int)(((uint32_t)(v[e] >> 32) - cmin) >> bshift);
+        tmp[atomicAdd(cur + bk, 1)] = v[e];
+      }
+    }
+  }
+  __syncthreads();  // cur = bucket ends (bucket b starts at cur[b - 1])
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 4] = clock64() - t_dbg0;
+  for (int w0 = 0; w0 < n;) {
+    // window end: the last bucket end <= w0 + WCAP (a bucket holds fewer
+    // than BK_BIG_G < WCAP keys, so the window is not empty)
+    int w1 = n;
+    if (w0 + WCAP < n) {
+      int b = -1;
+#pragma unroll
+      for (int step = GN / 2; step >= 1; step >>= 1)
+        if (cur[b + step] <= w0 + WCAP) b += step;
+      w1 = cur[b];
+    }
+    const int len = w1 - w0;
+#pragma unroll
+    for (int e = 0; e < WCAP / RS_T; ++e) {
+      const int j = threadIdx.x + e * RS_T;
+      if (j < len) wa[j] = __ldcg(tmp + w0 + j);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      const uint64_t v = wa[j];
+      const int bk = (int)(((uint32_t)(v >> 32) - cmin) >> bshift);
+      const int lo = (bk ? cur[bk - 1] : 0) - w0, hi = cur[bk] - w0;
+      int rank = lo;
+      for (int i = lo; i < hi; ++i) {
+        const uint64_t u = wa[i];
+        rank += (u < v) || (u == v && i < j);  // equal keys: seam duplicates
+      }
+      wb[rank] = v;
+    }
+    __syncthreads();
+    fix_coarse_ties(wb, len, A.key);  // a coarse-key run lies inside one bucket
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) g[w0 + j] = wb[j];
+    __syncthreads();
+    w0 = w1;
+  }
+  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 5] = clock64() - t_dbg0;
 }
 
 // Gather each tile's staged segments, sort them by (coarse depth, index),
@@ -373,7 +510,7 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   }
   uint64_t* g = A.pairs + s;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-  if (seg_fast && n <= RS_CAP) {
+  if (seg_fast) {
     // segment table in shared memory (the bucket counters' space, unused
     // until the histogram): offset, length, list position
     int* s_soff = (int*)(s_keys + 2 * RS_CAP);
@@ -390,40 +527,48 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
       }
     }
     __syncthreads();
-    // thread t gathers keys [t*per, t*per + per): one binary search over the
-    // segment positions for its first key, then it walks forward through the
-    // (on average longer than per) segments; all its loads are in flight
-    // together
-    const int per = (n + RS_T - 1) / RS_T;  // <= RS_E
-    const int j0 = tid * per;
-    uint64_t v[RS_E];
-    if (j0 < n) {
-      int l = 0;  // last segment with position <= j0
-      for (int step = 1 << (31 - __clz(nseg)); step >= 1; step >>= 1)
-        if (l + step < nseg && s_spre[l + step] <= j0) l += step;
-      int sbeg = s_spre[l], send = sbeg + s_slen[l], soff = s_soff[l];
+    // windows of RS_CAP keys (one for lists that fit shared memory, else
+    // written to the list in L2): warp w gathers the window's keys
+    // [32 per w, 32 per (w + 1)), lane l the keys 32 e + l of that block, so
+    // every load instruction reads consecutive keys; a lane binary-searches
+    // the segment positions for its first key and walks forward from there.
+    // All of a thread's loads are in flight together.
+    for (int w0 = 0; w0 < n; w0 += RS_CAP) {
+      const int nw = min(n - w0, RS_CAP);
+      const int per = (nw + RS_T - 1) / RS_T;  // <= RS_E
+      const int j0 = w0 + warp * 32 * per + lane, jend = w0 + nw;
+      uint64_t v[RS_E];
+      if (j0 < jend) {
+        int l = 0;  // last segment with position <= j0
+        for (int step = 1 << (31 - __clz(nseg)); step >= 1; step >>= 1)
+          if (l + step < nseg && s_spre[l + step] <= j0) l += step;
+        int sbeg = s_spre[l], send = sbeg + s_slen[l], soff = s_soff[l];
 #pragma unroll
-      for (int e = 0; e < RS_E; ++e) {
-        const int j = j0 + e;
-        v[e] = 0;
-        if (e < per && j < n) {
-          while (j >= send) {  // next non-empty segment
-            ++l;
-            sbeg = s_spre[l];
-            send = sbeg + s_slen[l];
-            soff = s_soff[l];
+        for (int e = 0; e < RS_E; ++e) {
+          const int j = j0 + 32 * e;
+          v[e] = 0;
+          if (e < per && j < jend) {
+            while (j >= send) {  // segment holding key j
+              ++l;
+              sbeg = s_spre[l];
+              send = sbeg + s_slen[l];
+              soff = s_soff[l];
+            }
+            v[e] = __ldcg(A.stage + soff + (j - sbeg));
           }
-          v[e] = __ldcg(A.stage + soff + (j - sbeg));
         }
-      }
 #pragma unroll
-      for (int e = 0; e < RS_E; ++e) {
-        const int j = j0 + e;
-        if (e < per && j < n) {
-          s_keys[j] = v[e];
-          const uint32_t c = (uint32_t)(v[e] >> 32);
-          lo = min(lo, c);
-          hi = max(hi, c);
+        for (int e = 0; e < RS_E; ++e) {
+          const int j = j0 + 32 * e;
+          if (e < per && j < jend) {
+            if (n <= RS_CAP)
+              s_keys[j] = v[e];
+            else
+              g[j] = v[e];
+            const uint32_t c = (uint32_t)(v[e] >> 32);
+            lo = min(lo, c);
+            hi = max(hi, c);
+          }
         }
       }
     }
@@ -494,33 +639,14 @@ __global__ void __launch_bounds__(RS_T) k_tile_sort(SortArgs A) {
   } else if (n == 1) {
     if (threadIdx.x == 0) g[0] = s_keys[0];
   } else if (n > RS_CAP) {
-    // longer than shared memory: the same bucket pass with the keys in L2
-    // (g and a scratch slice of the same offsets), the counters in shared
-    // memory; a bucket of >= BK_BIG_G keys falls back to a bitonic sort
     if (threadIdx.x == 0) atomicAdd(A.counters + GSPARC_CNT_BIGTILE, 1);
-    int* cnt = (int*)(s_keys + 2 * RS_CAP);
-    int* bcnt = cnt;
-    int* bcur = cnt + BK_N;
-    const uint32_t cmin = s_mm[0], span = s_mm[1] - s_mm[0];
-    const int bits = span ? 32 - __clz(span) : 0;
-    const int bshift = bits > BK_BITS ? bits - BK_BITS : 0;
-    __shared__ int s_gbig;
-    if (threadIdx.x == 0) s_gbig = 0;
-    for (int q = threadIdx.x; q < BK_N; q += blockDim.x) bcnt[q] = 0;
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const int bk = (int)(((uint32_t)(g[j] >> 32) - cmin) >> bshift);
-      if (atomicAdd(bcnt + bk, 1) == BK_BIG_G) s_gbig = 1;
-    }
-    __syncthreads();
-    if (!s_gbig && A.sort_tmp) {
-      bucket_pass(g, A.sort_tmp + s, bcnt, bcur, n, cmin, bshift);
-    } else {
-      bitonic_sort<false>(g, n);  // in place in global memory (L2 resident)
-      __syncthreads();
-    }
-    fix_coarse_ties(g, n, A.key);
-    __syncthreads();
+    // (2^15 + 1 cursors fit behind two half windows: 64 + 128 KB)
+    if (A.long_bits == 15)
+      sort_long_list<15>(A, s_keys, g, n, s, s_mm[0], s_mm[1], t_dbg0);
+    else if (A.long_bits == 14)
+      sort_long_list<14>(A, s_keys, g, n, s, s_mm[0], s_mm[1], t_dbg0);
+    else
+      sort_long_list<13>(A, s_keys, g, n, s, s_mm[0], s_mm[1], t_dbg0);
   }
   if (A.inv) {  // deterministic backward: list position of (Gaussian, tile slot)
     __syncthreads();
@@ -569,11 +695,12 @@ int launch_bin_tiles(const gsparc_frame_layout& L, char* frame, cudaStream_t st,
   A.ntx = L.ntx;
   A.ntiles = L.ntiles;
   A.dbg = nullptr;
+  A.long_bits = experiment_env("GSPARC_SORT_LBITS") ? atoi(experiment_env("GSPARC_SORT_LBITS")) : 14;
   if (experiment_env("GSPARC_SORT_DBG")) A.dbg = dbg_rows(0);  // experiments only
   const size_t cnt_ints =
-      (size_t)max(RS_W * 256 + 512, 2 * BK_N);
+      (size_t)max(RS_W * 256 + 512, 2 * BK_N + 1);
   const size_t smem_sort = 2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * cnt_ints;
-  static_assert(2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * 2 * BK_N <= 227 * 1024,
+  static_assert(2 * RS_CAP * sizeof(uint64_t) + sizeof(int) * (2 * BK_N + 1) <= 227 * 1024,
                 "k_tile_sort shared memory");
   static size_t attr_set = 0;
   if (attr_set < smem_sort) {
