@@ -510,6 +510,8 @@ struct PxbCfg {
   static constexpr int MAXREG = MIN_CTAS == 2 ? 128 : 224;
   static constexpr int PPR = NA * 8;                   // 16 B pieces per coef row
   static constexpr int NPF = (PX_K * PPR + 127) / 128; // pieces per group thread
+  static constexpr int EP_ROW = NP * 4 + 16;           // epilogue staging row (padded)
+  static constexpr int SMEM = (2 * STAGE > 128 * EP_ROW ? 2 * STAGE : 128 * EP_ROW) + 1024;
 };
 
 __device__ __forceinline__ uint32_t base32b_off(int k, int j, int na) {
@@ -860,9 +862,54 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     const long long te0 = clock64();
     if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 14] = te0 - t_start;
     const bool fast = (A.C % 8) == 0 && (A.Cp % 8) == 0;
+    const int ncol_cta = (int)min((int64_t)NP, A.Cp - col0);
+    // image rows through shared memory: when the CTA's columns are one
+    // contiguous run of every pixel's row (one TX, 16 B multiples), the
+    // accumulator goes TMEM -> shared memory (row per pixel, padded) and
+    // each pixel's run is written by one bulk copy -- full-line writes
+    // instead of 32 B pieces 4 C bytes apart
+    const bool bulk = nch > 0 && (A.C % 4) == 0 && (col0 % 4) == 0 && (ncol_cta % 4) == 0 &&
+                      col0 / A.C == (col0 + ncol_cta - 1) / A.C;
+    if (bulk) {
+      constexpr int RSB = CF::EP_ROW;  // row stride (bytes)
+      const int row = q * 32 + lane;
+      unsigned char* ep = sB + row * RSB;
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cend; c0 += 8) {
-      uint32_t v[8];
+      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        uint32_t v[8];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c0 < ncol_cta) {
+          uint4* d4 = (uint4*)(ep + 4 * c0);
+          d4[0] = make_uint4(v[0], v[1], v[2], v[3]);
+          if (c0 + 4 < ncol_cta) d4[1] = make_uint4(v[4], v[5], v[6], v[7]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+      // warp w copies pixels 16 w .. 16 w + 15 (TMEM lane = pixel)
+      if (lane < 16) {
+        const int r = 16 * warp + lane, rq = r >> 5, rl = r & 31;
+        const int bx = g.x0 + (rl & 15), by = g.y0 + 2 * rq + (rl >> 4);
+        if (bx < A.w && by < A.h) {
+          const int64_t b = col0 / A.C, ch = col0 - b * A.C;
+          float* dst = A.img + ((b * A.h + by) * (int64_t)A.w + bx) * A.C + ch;
+          asm volatile(
+              "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+              "r"(smem_u32(sB + r * RSB)), "r"(ncol_cta * 4)
+              : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+    } else {
+#pragma unroll 1
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {      uint32_t v[8];
       if (nch > 0) {
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
         asm volatile(
@@ -895,6 +942,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         }
       }
     }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -925,7 +973,7 @@ long long* dbg_rows(int which) {
 template <int NP>
 static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream_t st) {
   using CF = PxbCfg<NP>;
-  size_t smem = 2 * CF::STAGE + 1024;
+  size_t smem = CF::SMEM;
   // two CTAs per SM at most (TMEM); keep a third from being scheduled
   if (CF::MIN_CTAS == 2 && smem < 78 * 1024) smem = 78 * 1024;
   static bool attr = false;
