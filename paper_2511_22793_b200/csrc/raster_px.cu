@@ -909,7 +909,8 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       }
     } else {
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cend; c0 += 8) {      uint32_t v[8];
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      uint32_t v[8];
       if (nch > 0) {
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
         asm volatile(
