@@ -278,7 +278,10 @@ __global__ void k_loss_finalize(LossArgsT<T> A) {
 //     L1 term + magnitude chain -> dL/dimg.
 // Same arithmetic (f64, taps in order) as the per-pixel kernels above, two
 // launches instead of six.
-constexpr int LB = 32;        // output columns per band (the last band is padded)
+// 40-column bands: 9 bands x 32 planes = 288 CTAs of one per SM (2 waves
+// on 148 SMs) at 90x360, where 32 columns gave 384 (2.6 waves)
+constexpr int LB = 40;        // output columns per band (the last band is padded)
+constexpr int RB = 1024 / LB; // band rows per pass
 constexpr int XW = LB + 10;   // staged columns: the band + a 5-column halo each side
 
 __host__ __device__ inline int loss_nbands(int w) { return (w + LB - 1) / LB; }
@@ -288,7 +291,7 @@ __host__ __device__ inline size_t loss_band_smem(int h) {
 __host__ __device__ inline size_t loss_adj_smem(int h) {
   return sizeof(double) * (size_t)h * (size_t)(6 * XW);
 }
-constexpr size_t LOSS_SMEM_MAX = 200 * 1024;
+constexpr size_t LOSS_SMEM_MAX = 224 * 1024;  // + the static reduction buffer <= 227 KB
 
 // 11-tap window sum over a strided line with every tap in range
 __device__ __forceinline__ double tap11(const double (&wv)[11], const double* g, int stride) {
@@ -333,11 +336,11 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   // x / y with reflect-padded columns (columns past the image in a padded
   // last band are staged too; their outputs are never written)
   // 2-D thread maps fixed per thread (no index divisions in the loops):
-  // staged rows of XW columns (24 rows per pass) and band rows of LB columns
-  // (32 rows per pass)
-  constexpr int RS = 1024 / XW;  // 24
+  // staged rows of XW columns (RS rows per pass) and band rows of LB columns
+  // (RB rows per pass)
+  constexpr int RS = 1024 / XW;
   const int sx = threadIdx.x % XW, sy = threadIdx.x / XW;
-  const int bx = threadIdx.x & (LB - 1), by = threadIdx.x >> 5;
+  const int bx = threadIdx.x % LB, by = threadIdx.x / LB;
   if (sy < RS) {
     const int col = refl(min(c0 - 5 + sx, 2 * w - 1), w);
 #pragma unroll 4
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   }
   __syncthreads();
   const int HW = h * LB;
-  for (int r = by; r < h; r += 32) {
+  for (int r = by; r < h && by < RB; r += RB) {
     const int c = bx, e = r * LB + c;
     double a[5] = {0, 0, 0, 0, 0};
     const double* xr = X + r * XW + c;
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(1024) k_loss_band_fwd(LossArgsT<T> A) {
   __syncthreads();
   const int64_t plane = (int64_t)h * w, tot = (int64_t)A.NI * A.S * plane;
   double v3[3] = {0.0, 0.0, 0.0};
-  for (int r = by; r < h; r += 32) {
+  for (int r = by; r < h && by < RB; r += RB) {
     const int c = bx;
     if (c0 + c >= w) continue;
     double m[5] = {0, 0, 0, 0, 0};
@@ -436,9 +439,9 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
   double* G = lsm;                 // [3][h][XW], columns c0-5 .. c0+LB+5
   double* Av = G + 3 * h * XW;     // [3][h][XW]
   const int HX = h * XW;
-  constexpr int RS = 1024 / XW;  // 24 staged rows per pass
+  constexpr int RS = 1024 / XW;  // staged rows per pass
   const int sx = threadIdx.x % XW, sy = threadIdx.x / XW;
-  const int bx = threadIdx.x & (LB - 1), by = threadIdx.x >> 5;
+  const int bx = threadIdx.x % LB, by = threadIdx.x / LB;
   if (sy < RS) {
     const int col = c0 - 5 + sx;
     const bool in = col >= 0 && col < w;
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
   __syncthreads();
   const double n = (double)plane;
   const double inv_n = 1.0 / n, k_l1 = (1.0 - A.lam) / (n * A.S), k_ss = A.lam / A.S;
-  for (int r = by; r < h; r += 32) {
+  for (int r = by; r < h && by < RB; r += RB) {
     const int c = bx, col = c0 + c;
     if (col >= w) continue;
     const double* row = Av + r * XW;
@@ -489,15 +492,18 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
 
 template <typename T>
 __global__ void k_loss_band_finalize(LossArgsT<T> A, int nbands) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per image: lanes take the band partials (all loads in flight),
+  // then a fixed butterfly -- the same order on every run
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (b >= A.NI) return;
   const double n = (double)A.h * A.w;
   double ss = 0.0, l1s = 0.0, sqs = 0.0, ss0 = 0.0, sq0 = 0.0;
   for (int s = 0; s < A.S; ++s) {
     const double* sm = A.sums + ((int64_t)b * A.S + s) * nbands * 3;
     double t[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < nbands; ++k)
+    for (int k = lane; k < nbands; k += 32)
       for (int q = 0; q < 3; ++q) t[q] += sm[k * 3 + q];
+    for (int q = 0; q < 3; ++q) t[q] = warp_sum(t[q]);
     ss += t[0] / n;
     l1s += t[1];
     sqs += t[2];
@@ -506,6 +512,7 @@ __global__ void k_loss_band_finalize(LossArgsT<T> A, int nbands) {
       sq0 = t[2] / n;
     }
   }
+  if (lane) return;
   ss /= A.S;
   const double l1 = l1s / (n * A.S);
   double* o = A.stats + (int64_t)GSPARC_LOSS_STATS * b;
@@ -566,7 +573,7 @@ static int run_loss(const T* img, const T* gt, int NI, int h, int w, int C, int 
     const dim3 grid((unsigned)nb, (unsigned)(NI * A.S));
     k_loss_band_fwd<T><<<grid, 1024, loss_band_smem(h), st>>>(A);
     k_loss_band_adj<T><<<grid, 1024, loss_adj_smem(h), st>>>(A);
-    k_loss_band_finalize<T><<<(NI + 127) / 128, 128, 0, st>>>(A, nb);
+    k_loss_band_finalize<T><<<(NI + 3) / 4, 128, 0, st>>>(A, nb);
     return check_launch("k_loss_band");
   }
   const unsigned blocks = (unsigned)((tot + 255) / 256);
