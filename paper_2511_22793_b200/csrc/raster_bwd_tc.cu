@@ -203,6 +203,7 @@ struct BwdTcArgs {
   int Cp, C, Kp;
   int w, h, ntx;
   int det;
+  int lpt;  // longest-first CTA order
 };
 
 __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
@@ -210,7 +211,37 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   __shared__ TcShared S;
   if (A.counters[GSPARC_CNT_OVERFLOW]) return;
-  const int cta = blockIdx.x, tile = cta >> 1, half = cta & 1;
+  int cta = blockIdx.x;
+  if (A.lpt) {
+    // longest-first: CTAs are dispatched in blockIdx order, so block k takes
+    // the half tile with the k-th most entries to visit (ties by index);
+    // one CTA per SM, and the heavy half tiles no longer end the grid
+    __shared__ int s_item;
+    int* s_nv = (int*)sm;  // [gridDim.x], before any staging
+    const int nitem = gridDim.x;
+    for (int i = threadIdx.x; i < nitem; i += blockDim.x) {
+      const int t = i >> 1, hf = i & 1;
+      int nv = 0;
+      if ((t / A.ntx) * TILE + hf * 8 < A.h) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nv = max(nv, A.wstop[t * 8 + hf * 4 + q]);
+      }
+      s_nv[i] = nv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nitem; i += blockDim.x) {
+      const int v = s_nv[i];
+      int rank = 0;
+      for (int j = 0; j < nitem; ++j) {
+        const int u = s_nv[j];
+        rank += (u > v) || (u == v && j < i);
+      }
+      if (rank == (int)blockIdx.x) s_item = i;
+    }
+    __syncthreads();
+    cta = s_item;
+  }
+  const int tile = cta >> 1, half = cta & 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tx_ = tile % A.ntx, ty = tile / A.ntx;
   const int x0 = tx_ * TILE, y0 = ty * TILE + half * 8;
@@ -675,6 +706,9 @@ int launch_raster_bwd_tc(const gsparc_frame_layout& L, char* frame, int n_tx, in
   A.w = L.width;
   A.h = L.height;
   A.ntx = L.ntx;
+  static const int lpt =
+      experiment_env("GSPARC_K5_LPT") ? atoi(experiment_env("GSPARC_K5_LPT")) : 1;
+  A.lpt = lpt;
   A.det = det ? 1 : 0;
   static bool attr_set = false;
   if (!attr_set) {
