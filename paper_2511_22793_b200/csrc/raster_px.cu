@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     const int end = g.any ? len : 0;
     // software pipeline: list indices DI batches ahead, records DR batches
     // ahead (the record load depends on the index load)
-    constexpr int DI = 6, DR = 3;
+    constexpr int DI = 10, DR = 6;
     auto ld_idx = [&](int p) -> uint32_t {
       return p + lane < end ? (uint32_t)__ldcg(A.pairs + start + p + lane) : 0xffffffffu;
     };
