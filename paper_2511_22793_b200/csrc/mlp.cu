@@ -212,9 +212,11 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 14] = gtimer();
-  // streaming (render path): pass B may run its prologue (it waits for this
-  // grid).  Not otherwise: a pass A launched next would read coef early.
-  if (A.stream_ctas) pdl_trigger();
+  // pass B with several channel chunks (> 256 columns, config 5: thousands
+  // of CTAs) is scheduled from the MLP's start -- its first CTAs' prologues
+  // then overlap the whole MLP (measured 2% faster there); with one chunk
+  // only once pass A has finished (below)
+  if (A.stream_ctas && A.Cp > 256) pdl_trigger();
   if (A.live_list && A.stream_ctas) {
     // streaming: the list is -1 where pass A has not written yet (K2 clears
     // it); a warp takes entries wid, wid + nwarps, ... as they appear, and
@@ -236,6 +238,12 @@ __global__ void __launch_bounds__(256, 2) k_mlp_wide(MlpArgs A) {
       mlp_wide_one(A, v, lane);
       if (A.dbg && lane == 0) atomicMax(A.dbg + blockIdx.x * 16 + 13, (long long)gtimer());
     }
+    // this warp found the end of the live list (pass A has finished): pass B
+    // may now be scheduled and run its prologue beside the MLP's last
+    // Gaussians (it waits for this grid).  Not earlier -- its CTAs would sit
+    // on SMs pass A still needs -- and not in the other modes, where a pass A
+    // launched next would read coef early.
+    pdl_trigger();
     if (A.dbg) {
       __syncthreads();
       if (threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 15] = gtimer();

@@ -997,14 +997,12 @@ static void launch_pxb(const PxArgs& A, int chunks_y, bool after_mlp, cudaStream
   B.tile_major_b = chunks_y > 1 && tmaj && !B.mix_b;
   if (experiment_env("GSPARC_PXB_DBG")) B.dbg = dbg_rows(2);  // experiments only
   // dependent launch behind the streaming MLP (render path, pass 2): the
-  // prologue (TMEM allocation, barriers, stage clearing) overlaps the MLP's
-  // tail.  Measured: config 5 +4.7%, config 3 neutral; directly behind pass
-  // A (pass 0) the early CTAs only park on the SMs (config 1 -2.5%).
+  // MLP triggers once pass A has finished, so the prologue (TMEM allocation,
+  // barriers, stage clearing) overlaps the MLP's last Gaussians.  Directly
+  // behind pass A (pass 0) the early CTAs only park on the SMs (config 1
+  // -2.5%).
   static const bool pdl_env = !getenv("GSPARC_NO_PDL") && !experiment_env("GSPARC_NO_PDL_B");
-  // (one channel chunk, e.g. config 3: an ordinary launch with the reads
-  // ahead of the prologue is as fast)
-  static const bool pdl1 = experiment_env("GSPARC_PXB_PDL1") != nullptr;  // experiments
-  const bool pdl = pdl_env && after_mlp && (chunks_y > 1 || pdl1);
+  const bool pdl = pdl_env && after_mlp;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
   cfg.gridDim = dim3(A.ntiles * 2, chunks_y);
