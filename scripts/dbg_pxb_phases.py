@@ -1,3 +1,7 @@
+"""Pass-B per-chunk phase split (experiments, config 3).  Reads the
+GSPARC_PXB_DBG rows; the per-phase clock64 stamps it prints (slots 0-5, 8-9,
+12-13) were a temporary patch of k_pxb's chunk loop (see
+profiles/r02/SUMMARY.md), not kept in the kernel."""
 import ctypes, os, sys
 os.environ["GSPARC_PXB_DBG"] = "1"
 sys.path.insert(0, "/root/repo")
