@@ -430,14 +430,41 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   // live list (for the lazy MLP): entries of this CTA's chunks with an
   // included contribution; the first CTA to flag a Gaussian appends it.
   // Done once per CTA, off the per-chunk critical path.
+  // Loads, flag exchanges and list appends of up to LE entries per thread in
+  // flight together; one list reservation per warp and round.
   const int nused = s_nch * PX_K;
-  for (int t = threadIdx.x; t < nused; t += blockDim.x) {
-    const int c = t >> 5, e = t & 31;
-    const uint32_t used = __ldcg(A.ch_used + slot0 + c);
-    if ((used >> e) & 1u) {
-      const int idx = (int)__ldcg(A.ch_idx + (slot0 + c) * PX_K + e);
-      if (atomicExch(A.live + idx, 1) == 0) A.live_list[atomicAdd(A.counters + GSPARC_CNT_LIVE, 1)] = idx;
+  constexpr int LE = 4;
+  for (int t0 = threadIdx.x; t0 - (int)threadIdx.x < nused; t0 += LE * (int)blockDim.x) {
+    uint32_t used[LE];
+    int idx[LE];
+#pragma unroll
+    for (int k = 0; k < LE; ++k) {
+      const int t = t0 + k * blockDim.x, c = t >> 5;
+      used[k] = t < nused ? __ldcg(A.ch_used + slot0 + c) : 0u;
+      idx[k] = t < nused ? (int)__ldcg(A.ch_idx + (slot0 + c) * PX_K + (t & 31)) : -1;
     }
+    bool fresh[LE];
+#pragma unroll
+    for (int k = 0; k < LE; ++k) {
+      const int t = t0 + k * blockDim.x;
+      fresh[k] = ((used[k] >> (t & 31)) & 1u) && atomicExch(A.live + idx[k], 1) == 0;
+    }
+    int nf = 0;
+#pragma unroll
+    for (int k = 0; k < LE; ++k) nf += fresh[k];
+    int incl = nf;  // warp inclusive scan of the fresh counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((threadIdx.x & 31) >= o) incl += u;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    int base = 0;
+    if ((threadIdx.x & 31) == 31 && wtot) base = atomicAdd(A.counters + GSPARC_CNT_LIVE, wtot);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - nf;
+#pragma unroll
+    for (int k = 0; k < LE; ++k)
+      if (fresh[k]) A.live_list[base++] = idx[k];
   }
   // this CTA's live-list entries are written: count it finished (K1 stops
   // waiting for entries once every pass-A CTA has)
