@@ -29,6 +29,8 @@ STAGE = [  # (kernel-name regex, stage per config kind)
     (r"k_raster_bwd", "backward"),
     (r"k_gauss_bwd", "gauss_backward"),
     (r"k_adam", "adam"),
+    (r"k_loss_band_fwd", "loss_fwd"),
+    (r"k_loss_band_adj", "loss_adj"),
 ]
 DETAILS = {"Duration": "duration_us", "Issue Slots Busy": "issue_slots_busy_pct",
            "Achieved Occupancy": "achieved_occupancy_pct",
