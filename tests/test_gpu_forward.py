@@ -224,22 +224,33 @@ def test_sort_exact_depth_ties(R, pose):
     assert_image_parity(img.data, ref, aux.contrib_count, aux_ref.contrib_count, F32_TOL)
 
 
-def test_sort_tile_beyond_shared_memory(R, pose):
-    """A tile list longer than K3's shared-memory capacity (8192 keys) takes
-    the in-L2 bitonic path; lists stay bit-exact."""
-    from paper_2511_22793_b200 import _lib
-    rng = np.random.default_rng(11)
-    n = 9000
-    # small Gaussians in front of one tile of a 64x32 image, spread in depth
+def _long_list_scene(n, n_dup, seed):
+    """n small Gaussians in front of one tile of a 64x32 image, spread in
+    depth, plus n_dup copies of one of them (identical depth keys)."""
+    rng = np.random.default_rng(seed)
     u = rng.uniform(8.0, 16.0, n)
     v = rng.uniform(2.0, 10.0, n)
     dirs = np.stack([O.pixel_dir(int(a) % 64, int(b) % 32, 64, 32)
                      for a, b in zip(u, v)])
     r = rng.uniform(1.0, 6.0, n)[:, None]
     base = O.make_uniform([-1, 0, -1], [1, 1, 1], n, seed=5, init_scale=0.02)
-    oc = O.Cloud(dirs * r, base.log_scales, base.rotations, base.raw_opacities - 1.0,
-                 base.mlp_weights * 0.3, mlp_dims=base.mlp_dims)
-    oc = O.round_f32(oc)
+    pos = dirs * r
+    take = lambda a: np.concatenate([a, np.repeat(a[:1], n_dup, 0)]) if n_dup else a
+    oc = O.Cloud(take(pos), take(base.log_scales), take(base.rotations),
+                 take(base.raw_opacities - 1.0), take(base.mlp_weights * 0.3),
+                 mlp_dims=base.mlp_dims)
+    return O.round_f32(oc)
+
+
+@pytest.mark.parametrize("n,n_dup", [(9000, 0), (20000, 0), (12000, 300)])
+def test_sort_tile_beyond_shared_memory(n, n_dup, R, pose):
+    """Tile lists longer than K3's shared-memory capacity (8192 keys): the
+    gather in 8192-key windows to L2, the 2^14-bucket pass with the keys in
+    L2 and whole-bucket windows ranked in shared memory (9000: two windows,
+    20000: three); 300 identical keys fill one bucket past 256 and take the
+    in-L2 bitonic fallback.  Lists stay bit-exact."""
+    from paper_2511_22793_b200 import _lib
+    oc = _long_list_scene(n, n_dup, 11)
     tx = O.sample_tx(4, 1)[0]
     ref, aux_ref = O.forward(oc, RX, W, tx, 64, 32, threads=8)
     assert max(len(v) for v in aux_ref.tiles.values()) > 8192
