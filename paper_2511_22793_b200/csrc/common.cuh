@@ -294,6 +294,16 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Visited list prefix of sub-tile `part` (of nsub = 2 or 4 row bands) of a
+// tile, for the backward: the max of the forward's per-warp prefixes
+// (wstop, 8 per tile) over the part's half tile.  Pass A's warp w holds rows
+// {w, 7 - w} of a half (raster_px.cu half_row), so every 4-row band meets all
+// four of the half's warps; the f64 path's 2-row strips are bounded too.
+__device__ __forceinline__ int part_nvisit(const int* wstop, int tile, int part, int nsub) {
+  const int* w = wstop + tile * 8 + ((part * 2) / nsub) * 4;
+  return max(max(w[0], w[1]), max(w[2], w[3]));
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_raster_bwd(BwdArgs A) {
   const int py = ty * TILE + part * A.sr + pix / TILE;
   const bool inside = px < A.w && py < A.h;
   const int start = A.tile_start[tile], tile_end = A.tile_start[tile + 1];
-  const int nvisit = max(A.wstop[tile * 8 + part * 2], A.wstop[tile * 8 + part * 2 + 1]);
+  const int nvisit = part_nvisit(A.wstop, tile, part, A.nsub);
   if (nvisit == 0) return;
   const int chunk_base = chunk * CB;
   const R pcx = (R)px + R(0.5), pcy = (R)py + R(0.5);
@@ -414,12 +414,10 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(RedArgs A) {
       // which (copy, sub-tile) partials exist: K5 wrote those inside each
       // sub-tile's visited prefix (wstop, per 32-pixel warp)
       const int ts = A.tile_start[t];
-      const int wpp = 8 / A.nsub;  // 32-pixel warps (wstop entries) per sub-tile
       unsigned vis = 0;
       for (int copy = 0; copy <= (twice ? 1 : 0); ++copy)
         for (int p = 0; p < A.nsub; ++p) {
-          int nv = 0;
-          for (int q = 0; q < wpp; ++q) nv = max(nv, A.wstop[t * 8 + p * wpp + q]);
+          const int nv = part_nvisit(A.wstop, t, p, A.nsub);
           if (lo + copy - ts < nv) vis |= 1u << (4 * copy + p);
         }
       s_vis[warp][jj] = (unsigned char)vis;

@@ -115,6 +115,14 @@ __device__ __forceinline__ int64_t chunk_slot0(const int* tile_start, int tile, 
   return 2 * ((s + 31 * (int64_t)tile) >> 5) + half * ((len + 31) >> 5);
 }
 
+// Pixel row (0..7) of a half tile held by lane group hi (lane >> 4) of the
+// 32-pixel warp w: rows {w, 7 - w}, so every warp has one row of each end of
+// the half tile (per-pixel list lengths change monotonically across a tile
+// near the poles; rows {2w, 2w + 1} left one warp with both heavy rows).
+// Pass A, pass B and pass B's epilogue share it (stored weights, T
+// checkpoints and TMEM lanes are indexed by warp * 32 + lane).
+__device__ __forceinline__ int half_row(int w, int hi) { return hi ? 7 - w : w; }
+
 struct CtaGeom {
   int tile, half, x0, y0;
   float xc, xhalf, ylo, yhi;
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     }
   } else {
     // ---------------- consumers: one pixel per lane
-    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * warp + (lane >> 4);
+    const int px = g.x0 + (lane & 15), py = g.y0 + half_row(warp, lane >> 4);
     const bool inside = px < A.w && py < A.h;
     const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
     const float teps = A.t_eps, wf = A.wf, inv_w = A.inv_w;
@@ -647,7 +655,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
   if (warp < 8) {
     // ---------------- weight groups: group gq takes chunks c = gq (mod 2)
     const int gq = warp >> 2, q = warp & 3, gt = q * 32 + lane;  // thread in group
-    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
+    const int px = g.x0 + (lane & 15), py = g.y0 + half_row(q, lane >> 4);
     const float pcx = (float)px + 0.5f, pcy = (float)py + 0.5f;
     const float teps = A.t_eps, wf = A.wf, inv_w = A.inv_w;
     float4* rs = s_rec[warp];
@@ -880,7 +888,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
     constexpr int NPH = ((NP / 2 + 7) / 8) * 8;
     const int q = warp & 3;
     const int cbeg = warp < 4 ? 0 : NPH, cend = warp < 4 ? NPH : NP;
-    const int px = g.x0 + (lane & 15), py = g.y0 + 2 * q + (lane >> 4);
+    const int px = g.x0 + (lane & 15), py = g.y0 + half_row(q, lane >> 4);
     const bool inside = px < A.w && py < A.h;
     if (nch > 0) {
       mbar_wait_sleep(&s_done, 0);
@@ -922,7 +930,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
       // warp w copies pixels 16 w .. 16 w + 15 (TMEM lane = pixel)
       if (lane < 16) {
         const int r = 16 * warp + lane, rq = r >> 5, rl = r & 31;
-        const int bx = g.x0 + (rl & 15), by = g.y0 + 2 * rq + (rl >> 4);
+        const int bx = g.x0 + (rl & 15), by = g.y0 + half_row(rq, rl >> 4);
         if (bx < A.w && by < A.h) {
           const int64_t b = col0 / A.C, ch = col0 - b * A.C;
           float* dst = A.img + ((b * A.h + by) * (int64_t)A.w + bx) * A.C + ch;
