@@ -967,6 +967,18 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
                              __uint_as_float(v[3]));
         dst[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]),
                              __uint_as_float(v[7]));
+      } else if ((A.C & 1) == 0 && (A.Cp & 1) == 0) {
+        // even channel counts (config 1: 64 TX x 2): channel pairs as 8 B
+        // stores -- a warp's 16 pixels of a row write 16 C contiguous bytes
+#pragma unroll
+        for (int jx = 0; jx < 8; jx += 2) {
+          const int64_t cc = cc0 + jx;
+          if (cc < A.Cp) {
+            const int64_t b = cc / A.C, ch = cc - b * A.C;
+            *(float2*)(A.img + ((b * A.h + py) * (int64_t)A.w + px) * A.C + ch) =
+                make_float2(__uint_as_float(v[jx]), __uint_as_float(v[jx + 1]));
+          }
+        }
       } else {
 #pragma unroll
         for (int jx = 0; jx < 8; ++jx) {
