@@ -8,6 +8,8 @@
 // f64 throughout (variance terms cancel).  Pipeline, one thread per pixel:
 //   h-blur of (x, y, xx, yy, xy) -> v-blur + SSIM map + adjoint seeds
 //   -> adjoint v -> adjoint h + L1 term + magnitude chain -> dimg.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -52,7 +54,11 @@ __device__ __forceinline__ int refl(int j, int n) {
 template <typename T>
 __device__ __forceinline__ double pred_at(const LossArgsT<T>& A, int b, int s, int r, int c) {
   const T* z = A.img + (((int64_t)b * A.h + r) * A.w + c) * A.C;
-  if (A.sup == 0) return hypot((double)z[0], (double)z[1]);
+  if (A.sup == 0) {  // C == 2: one (re, im) pair load
+    using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+    const T2 zz = *(const T2*)z;
+    return hypot((double)zz.x, (double)zz.y);
+  }
   return (double)z[s];
 }
 template <typename T>
@@ -477,13 +483,16 @@ __global__ void __launch_bounds__(1024) k_loss_band_adj(LossArgsT<T> A) {
     const double sgn = diff > 0 ? 1.0 : (diff < 0 ? -1.0 : 0.0);
     const double gp = sgn * k_l1 - k_ss * gssim;
     T* dz = A.dimg + (((int64_t)b * h + r) * w + col) * A.C;
-    if (A.sup == 0) {
-      const T* z = A.img + (((int64_t)b * h + r) * w + col) * A.C;
-      const double re = z[0], im = z[1];
+    if (A.sup == 0) {  // (re, im) pairs: one 2-element load and store per pixel
+      using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+      const T2 zz = *(const T2*)(A.img + (((int64_t)b * h + r) * w + col) * A.C);
+      const double re = zz.x, im = zz.y;
       const double m = hypot(re, im);
       const double kk = m > 0.0 ? gp / m : 0.0;
-      dz[0] = (T)(re * kk);
-      dz[1] = (T)(im * kk);
+      T2 o;
+      o.x = (T)(re * kk);
+      o.y = (T)(im * kk);
+      *(T2*)dz = o;
     } else {
       dz[s] = (T)gp;
     }
