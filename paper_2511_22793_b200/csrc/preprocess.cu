@@ -78,7 +78,7 @@ __device__ __forceinline__ void for_big_tiles(unsigned bigm, int ry0, int ry1, i
 // {offset, length} per tile into its own slot and scatters its packed pairs
 // (coarse depth << 32 | index).  Order inside a tile is irrelevant: K3 sorts
 // each tile's gathered segments by the full key.
-__global__ void __launch_bounds__(PREP_T) k_preprocess(PrepArgs A) {
+__global__ void __launch_bounds__(PREP_T, 4) k_preprocess(PrepArgs A) {
   extern __shared__ int s_tiles[];  // per-CTA tile histogram [ntiles], offsets [ntiles+1], tmp
   const int ntiles = A.gc.ntx * A.gc.nty;
   int* s_off = s_tiles + ntiles;
