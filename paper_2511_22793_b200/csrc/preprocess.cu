@@ -373,28 +373,74 @@ __global__ void __launch_bounds__(PREP_T, 4) k_preprocess(PrepArgs A) {
   const unsigned bigm = __ballot_sync(0xffffffffu, kept_out && np_out > A.bin_small);
   for_big_tiles(bigm, ry0, ry1, ra0, ra1, rb0, rb1, packed, lane, A.gc.ntx,
                 [&](int t, uint64_t) { atomicAdd(s_tiles + t, 1); });
+  // this CTA's pair count: per-warp sums now, reserved in the global pair
+  // buffer (one returning atomic) while the tile scan runs
+  __shared__ int s_wnp[PREP_T / 32], s_wt[PREP_T / 32], s_total;
+  {
+    const int wnp = __reduce_add_sync(0xffffffffu, kept_out ? np_out : 0);
+    if (lane == 0) s_wnp[threadIdx.x >> 5] = wnp;
+  }
   __syncthreads();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 9] = clock64() - t_d0;  // rect+hist
-  block_exclusive_scan(s_tiles, s_off, ntiles, s_tmp);  // ends with a barrier
-  if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 10] = clock64() - t_d0;
-  const int total = s_off[ntiles];
-  if (threadIdx.x == 0) {
-    const int base = total ? atomicAdd(A.counters + GSPARC_CNT_PAIRS, total) : 0;
-    s_base = base;
-    if ((int64_t)base + total > A.capacity) A.counters[GSPARC_CNT_OVERFLOW] = 1;
+  bool fits;
+  if (ntiles <= PREP_T) {
+    // one tile per thread: warp scan of the histogram, warp totals in shared
+    // memory, one barrier (shared with the reservation's broadcast)
+    const int w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+      int total = 0;
+#pragma unroll
+      for (int k = 0; k < PREP_T / 32; ++k) total += s_wnp[k];
+      const int base = total ? atomicAdd(A.counters + GSPARC_CNT_PAIRS, total) : 0;
+      s_base = base;
+      s_total = total;
+      if ((int64_t)base + total > A.capacity) A.counters[GSPARC_CNT_OVERFLOW] = 1;
+    }
+    const int t = threadIdx.x;
+    const int v = t < ntiles ? s_tiles[t] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_wt[w] = inc;
+    __syncthreads();
+    int pre = 0;
+#pragma unroll
+    for (int k = 0; k < PREP_T / 32; ++k) pre += k < w ? s_wt[k] : 0;
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 10] = clock64() - t_d0;
+    const int base = s_base;
+    fits = (int64_t)base + s_total <= A.capacity;
+    // segment slot = this CTA's index (no returning atomics); empty
+    // segments have length 0
+    if (t < ntiles) {
+      const int off = base + pre + inc - v;
+      if (v) atomicAdd(A.tile_count + t, v);
+      if (fits) A.seg[(int64_t)t * A.seg_stride + blockIdx.x] = make_int2(off, v);
+      s_off[t] = off;
+    }
+    __syncthreads();
+  } else {
+    block_exclusive_scan(s_tiles, s_off, ntiles, s_tmp);  // ends with a barrier
+    if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 10] = clock64() - t_d0;
+    const int total = s_off[ntiles];
+    if (threadIdx.x == 0) {
+      const int base = total ? atomicAdd(A.counters + GSPARC_CNT_PAIRS, total) : 0;
+      s_base = base;
+      if ((int64_t)base + total > A.capacity) A.counters[GSPARC_CNT_OVERFLOW] = 1;
+    }
+    __syncthreads();
+    const int base = s_base;
+    fits = (int64_t)base + total <= A.capacity;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+      const int v = s_tiles[t];
+      if (v) atomicAdd(A.tile_count + t, v);
+      if (fits) A.seg[(int64_t)t * A.seg_stride + blockIdx.x] = make_int2(base + s_off[t], v);
+      s_off[t] += base;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const int base = s_base;
-  const bool fits = (int64_t)base + total <= A.capacity;
-  // segment slot = this CTA's index (no returning atomics); empty
-  // segments have length 0
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    const int v = s_tiles[t];
-    if (v) atomicAdd(A.tile_count + t, v);
-    if (fits) A.seg[(int64_t)t * A.seg_stride + blockIdx.x] = make_int2(base + s_off[t], v);
-    s_off[t] += base;
-  }
-  __syncthreads();
   if (A.dbg && threadIdx.x == 0) A.dbg[blockIdx.x * 16 + 11] = clock64() - t_d0;
   if (fits)
     for_big_tiles(bigm, ry0, ry1, ra0, ra1, rb0, rb1, packed, lane, A.gc.ntx,
