@@ -631,10 +631,6 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
                  "r"(CF::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
-  // unloaded rows keep whatever the stage held: start from zeros (finite)
-  for (int t = threadIdx.x; t < 2 * CF::STAGE / 16; t += blockDim.x)
-    ((float4*)sB)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -808,12 +804,14 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
         tmem_st16(a_hi + 16 * hh, hi);
         tmem_st16(a_lo + 16 * hh, lo);
       }
-      // coef hi/lo planes of the loaded rows (other rows untouched)
+      // coef hi/lo planes: every row of a K-step the MMAs read (8 entries
+      // with at least one loaded row), unloaded rows as zeros (cv = 0), so
+      // the stage never feeds stale or uninitialised data to a used K-step
 #pragma unroll
       for (int u = 0; u < CF::NPF; ++u) {
         const int p = gt + 128 * u;
         const int e = p / CF::PPR, jj = p - e * CF::PPR;
-        if (e < PX_K && ((lm >> e) & 1u) && jj < ppr) {
+        if (e < PX_K && ((lm >> (e & ~7)) & 0xFFu) && jj < ppr) {
           const float4 x = cv[u];
           float4 h;
           h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
