@@ -244,6 +244,13 @@ __device__ __forceinline__ float fast_alpha_uncut(float pcx, float pcy, float4 r
   return fminf(ex2_approx(fmaf(dx, t, fmaf(r1.x * dy, dy, r1.y))), ALPHA_MAX_F);
 }
 
+__device__ __forceinline__ float fast_alpha_shift(float pcx, float pcy, float4 r0, float4 r1) {
+  const float dx = (pcx - r0.x) + r1.w;
+  const float dy = pcy - r0.y;
+  const float t = fmaf(r0.w, dy, r0.z * dx);
+  return fminf(ex2_approx(fmaf(dx, t, fmaf(r1.x * dy, dy, r1.y))), ALPHA_MAX_F);
+}
+
 __device__ __forceinline__ float fast_alpha(float pcx, float pcy, float4 r0, float4 r1, float w,
                                             float inv_w) {
   const float dxr = pcx - r0.x;

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   __shared__ __align__(16) float4 s_ring[PX_RING][PX_K][2];
   __shared__ __align__(16) float s_cf[PX_RING][PX_K][SCW];
   __shared__ int s_hdr[PX_RING];
+  __shared__ int s_wrap[PX_RING];  // chunk holds an entry whose wrap varies across the CTA
   __shared__ __align__(8) uint64_t s_full[PX_RING], s_empty[PX_RING];
   __shared__ int s_ndone, s_nch, s_stop[4];
 
@@ -224,6 +225,9 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     // ---------------- producer: scan, cull, compact into the ring
     const unsigned lt = (1u << lane) - 1u;
     int c = 0, fill = 0, acquired = 0;
+    int wrap_c = 0, wrap_n = 0;  // wrap flags of chunks c and c + 1
+    // first and last pixel-centre column of the CTA (pass A's pcx values)
+    const float pxlo = g.x0 + 0.5f, pxhi = (float)min(g.x0 + TILE, A.w) - 0.5f;
     long long tpe = 0;
     auto acquire = [&](int k) {
       if (k > acquired) {
@@ -238,6 +242,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       if (lane == 0) {
         if (n > 0) A.ch_used[slot0 + k] = 0u;  // consumers OR their masks in
         s_hdr[k % PX_RING] = n;
+        s_wrap[k % PX_RING] = wrap_c;
         mbar_arrive(&s_full[k % PX_RING]);
       }
     };
@@ -279,6 +284,18 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int ns = __popc(m);
+      // azimuth wrap of the entry over the CTA: rint((pcx - mx) / w) is
+      // monotone in pcx, so equal values at the two end columns make it
+      // uniform, and the consumers add the exact shift -w k instead
+      // (fmaf(-w, k, dxr) == dxr + (-w k): the product is exact); a chunk
+      // with a non-uniform entry takes the per-pixel wrap
+      const float k_lo = rintf((pxlo - r0.x) * A.inv_w), k_hi = rintf((pxhi - r0.x) * A.inv_w);
+      {
+        const bool wr = keep && k_lo != k_hi;
+        const bool second = fill + __popc(m & lt) >= PX_K;
+        wrap_c |= __any_sync(0xffffffffu, wr && !second);
+        wrap_n |= __any_sync(0xffffffffu, wr && second);
+      }
       acquire(c);
       if (fill + ns > PX_K) acquire(c + 1);
       if (keep) {
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         const float4 r1p =
             make_float4(r1.x, r1.y, __int_as_float(pos + lane), __int_as_float((int)idx));
         s_ring[k % PX_RING][e][0] = r0;
-        s_ring[k % PX_RING][e][1] = r1p;
+        s_ring[k % PX_RING][e][1] = make_float4(r1.x, r1.y, r1p.z, -A.wf * k_lo);
         if (SC) {
 #pragma unroll
           for (int ch = 0; ch < SCW; ++ch)
@@ -306,12 +323,14 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         publish(c, PX_K);
         ++c;
         fill -= PX_K;
+        wrap_c = wrap_n;
+        wrap_n = 0;
       }
     }
     if (fill > 0) {  // zero-opacity padding: alpha = 0, never included
       if (lane >= fill) {
         s_ring[c % PX_RING][lane][0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_ring[c % PX_RING][lane][1] = make_float4(0.f, -INFINITY, __int_as_float(-1), __int_as_float(-1));
+        s_ring[c % PX_RING][lane][1] = make_float4(0.f, -INFINITY, __int_as_float(-1), 0.f);
         if (SC) {
 #pragma unroll
           for (int ch = 0; ch < SCW; ++ch) s_cf[c % PX_RING][lane][ch] = 0.f;
@@ -365,24 +384,35 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         unsigned actm = 0;
         float Tl = T;
         float wq[PX_K];
+        // the ring's r1.w holds the entry's azimuth shift -w k when the
+        // chunk's wraps are uniform over the CTA (s_wrap == 0): same bits as
+        // the per-pixel wrap, three instructions fewer per entry
+        auto walk = [&](auto uniform_tag) {
+          constexpr bool UNI = decltype(uniform_tag)::value;
 #pragma unroll
-        for (int k = 0; k < PX_K; ++k) {
-          const float4 r0 = s_ring[s][k][0], r1 = s_ring[s][k][1];
-          const float a = fast_alpha_uncut(pcx, pcy, r0, r1, wf, inv_w);
-          const bool act = Tl >= teps && a >= ALPHA_MIN_F;  // = fast_alpha(..) > 0
-          const float wgt = act ? Tl * a : 0.f;
-          if (SC) {
-            const float4 cf = *(const float4*)&s_cf[s][k][0];
-            acc[0] = fmaf(wgt, cf.x, acc[0]);
-            if (SC > 1) acc[1] = fmaf(wgt, cf.y, acc[1]);
-            if (SC > 2) acc[2] = fmaf(wgt, cf.z, acc[2]);
-            if (SC > 3) acc[3] = fmaf(wgt, cf.w, acc[3]);
-          } else {
-            wq[k] = wgt;
+          for (int k = 0; k < PX_K; ++k) {
+            const float4 r0 = s_ring[s][k][0], r1 = s_ring[s][k][1];
+            const float a = UNI ? fast_alpha_shift(pcx, pcy, r0, r1)
+                                : fast_alpha_uncut(pcx, pcy, r0, r1, wf, inv_w);
+            const bool act = Tl >= teps && a >= ALPHA_MIN_F;  // = fast_alpha(..) > 0
+            const float wgt = act ? Tl * a : 0.f;
+            if (SC) {
+              const float4 cf = *(const float4*)&s_cf[s][k][0];
+              acc[0] = fmaf(wgt, cf.x, acc[0]);
+              if (SC > 1) acc[1] = fmaf(wgt, cf.y, acc[1]);
+              if (SC > 2) acc[2] = fmaf(wgt, cf.z, acc[2]);
+              if (SC > 3) acc[3] = fmaf(wgt, cf.w, acc[3]);
+            } else {
+              wq[k] = wgt;
+            }
+            Tl = act ? fmaf(-Tl, a, Tl) : Tl;  // T (1 - alpha), one rounding
+            actm |= act ? (1u << k) : 0u;
           }
-          Tl = act ? fmaf(-Tl, a, Tl) : Tl;  // T (1 - alpha), one rounding
-          actm |= act ? (1u << k) : 0u;
-        }
+        };
+        if (s_wrap[s])
+          walk(std::integral_constant<bool, false>());
+        else
+          walk(std::integral_constant<bool, true>());
         T = Tl;
         if (actm) {
           cnt += __popc(actm);
@@ -938,7 +968,7 @@ __global__ void __launch_bounds__(PxbCfg<NP>::THREADS) __maxnreg__(PxbCfg<NP>::M
               : "memory");
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read out
       }
     } else {
 #pragma unroll 1
