@@ -80,6 +80,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-buffers", type=int, default=3,
+                    help="render e2e: device/pinned image buffers in flight")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--deterministic", action="store_true",
                     help="c2: fixed-order (bit-reproducible) backward")
@@ -574,23 +576,26 @@ def run_ours(args):
     # render i+1 -- what a serving loop would do.  Every render's TX is
     # copied in from pinned memory and every image lands in pinned memory
     # inside the timed region.
-    pin_tx = [torch.empty((B, 3), dtype=torch.float64).pin_memory() for _ in range(2)]
-    pin_img = [torch.empty((B, h, w, C), dtype=torch.float32).pin_memory() for _ in range(2)]
-    dev_img = [img, torch.empty_like(img)]
+    # NB image buffers in flight (render i reuses buffer i mod NB once its
+    # copy from render i - NB has finished)
+    NB = args.e2e_buffers
+    pin_tx = [torch.empty((B, 3), dtype=torch.float64).pin_memory() for _ in range(NB)]
+    pin_img = [torch.empty((B, h, w, C), dtype=torch.float32).pin_memory() for _ in range(NB)]
+    dev_img = [img] + [torch.empty_like(img) for _ in range(NB - 1)]
     copy_stream = torch.cuda.Stream()
-    rendered = [torch.cuda.Event() for _ in range(2)]
-    copied = [torch.cuda.Event() for _ in range(2)]
+    rendered = [torch.cuda.Event() for _ in range(NB)]
+    copied = [torch.cuda.Event() for _ in range(NB)]
     e2e_steps = min(args.steps, 100)
-    checks = [None, None]
+    checks = [None] * NB
 
     def e2e_run(n):
         for i in range(n):
-            k = i & 1
+            k = i % NB
             t = i % total_steps
             pin_tx[k].copy_(torch.as_tensor(txs_np[t * B:(t + 1) * B]))
             stream.wait_event(copied[k])          # image buffer k is free again
             tx_dev = pin_tx[k].to("cuda", non_blocking=True)
-            # deferred overflow check: verified two renders later, when
+            # deferred overflow check: verified NB renders later, when
             # buffer k is reused (re-rendered on the rare overflow)
             if checks[k] is not None and not checks[k].ok():
                 raise RuntimeError("pair buffer overflow in the e2e loop")
@@ -679,7 +684,8 @@ def run_ours(args):
                             "sync=False: each render's overflow flag read back "
                             "with it and checked before its buffer is reused) "
                             "+ D2H of every image into pinned memory on a copy "
-                            "stream overlapping the next render"},
+                            "stream overlapping the next render",
+                    "image_buffers": NB},
             "gpu_launches": int(args.steps * per_step_launches),
             "roofline": roof,
             "pipeline_hbm": {"algorithmic_bytes": bytes_fwd,

@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
   } else if (A.counters[GSPARC_CNT_OVERFLOW]) {
     return;
   }
-  if (A.dbg && threadIdx.x == 0) A.dbg[cta * 16 + 14] = gtimer();
+  if (A.dbg && threadIdx.x == 0) {
+    A.dbg[cta * 16 + 13] = clock64() - t_startA;  // tile claimed
+    A.dbg[cta * 16 + 14] = gtimer();
+  }
   pdl_trigger();  // the lazy MLP (K1) may start and consume the live list as it grows
   const CtaGeom g = cta_geom(A, cta);
   // the tile's bounds and list were written by a grid that may still be

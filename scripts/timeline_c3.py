@@ -70,3 +70,9 @@ for t in np.argsort(-np.maximum(a1[0::2], a1[1::2]))[:12]:
     print(t, ln[t], "[%.1f %.1f]" % (s0[t], s1[t]),
           "[%.1f %.1f] [%.1f %.1f]" % (a0[2 * t], a1[2 * t], a0[2 * t + 1], a1[2 * t + 1]),
           da[2 * t:2 * t + 2, 12], ((db[2 * t:2 * t + 2, 15] - db[2 * t:2 * t + 2, 12]) / 1e3).round(1))
+# pass A: consumers finished (stamp 11, cycles after the CTA start) -> CTA end
+# (live-list append, completion count, final grid wait)
+cons = a0 + (da[:, 11] - da[:, 13]) / 1965.0
+tail = a1 - cons
+print("pass A consumers done -> CTA end (live-list append): max %.1f mean %.1f us; latest consumer end %.1f, latest CTA end %.1f"
+      % (tail.max(), tail.mean(), cons.max(), a1.max()))
