@@ -154,6 +154,50 @@ __device__ __forceinline__ bool cull_keep(float4 r0, float4 r1, const CtaGeom& g
   return r1.z >= 0.f && dx <= r1.z && dy <= r1.w;
 }
 
+// Tighter, still conservative cull: the largest exponent
+//   q'(dx, dy) + log2(op),  q' = qa dx^2 + qb dx dy + qc dy^2  (concave)
+// over the continuous rectangle spanned by the CTA's pixel centres is below
+// log2(1/255) by a margin, so alpha < 1/255 at every pixel centre and the
+// entry is never included (skipping it is exact, as for cull_keep).  The
+// ellipse's bounding box (cull_keep) admits many such entries near the poles,
+// where footprints are wide and sheared.  The maximum is 0 when the rectangle
+// holds the centre, else on an edge (a 1-D concave quadratic, clamped).  The
+// margin covers the f32 rounding of this and of the per-pixel evaluation;
+// NaN, degenerate conics and azimuth wraps that differ across the CTA keep
+// the entry.
+__device__ __forceinline__ bool tight_keep(float4 r0, float4 r1, float xlo, float xhi, float ylo,
+                                           float yhi, float w, float inv_w) {
+  const float klo = rintf((xlo - r0.x) * inv_w), khi = rintf((xhi - r0.x) * inv_w);
+  const float qa = r0.z, qb = r0.w, qc = r1.x;
+  if (klo != khi || !(qa < 0.f && qc < 0.f)) return true;
+  const float x0 = (xlo - r0.x) - w * klo, x1 = (xhi - r0.x) - w * klo;
+  const float y0 = ylo - r0.y, y1 = yhi - r0.y;
+  // The maximum lies on an edge facing the centre (its supporting line
+  // separates the centre from the rectangle; a linear map preserves that),
+  // so at most one x edge and one y edge are candidates.  The clamped
+  // 1-D argmax uses fast reciprocals: a point near the argmax undershoots
+  // the edge maximum only by |q| delta^2, far inside the margin.
+  const bool ox = x0 > 0.f || x1 < 0.f, oy = y0 > 0.f || y1 < 0.f;
+  float m = 0.f;
+  if (ox || oy) {
+    const float xe = x0 > 0.f ? x0 : x1, ye = y0 > 0.f ? y0 : y1;
+    float rqa, rqc;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rqa) : "f"(qa));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rqc) : "f"(qc));
+    const float ys = fminf(fmaxf(-0.5f * qb * xe * rqc, y0), y1);
+    const float xs = fminf(fmaxf(-0.5f * qb * ye * rqa, x0), x1);
+    const float fx = fmaf(xe, fmaf(qa, xe, qb * ys), qc * ys * ys);
+    const float fy = fmaf(xs, fmaf(qa, xs, qb * ye), qc * ye * ye);
+    m = fmaxf(ox ? fx : -INFINITY, oy ? fy : -INFINITY);
+  }
+  // margin: 0.05 plus 2e-5 of the largest term magnitude over the rectangle
+  // (f32 rounding of the terms, and of dx: 1 ulp x |dq'/ddx| <= 2 |qa| X ulp)
+  const float X = fmaxf(fabsf(x0), fabsf(x1)), Y = fmaxf(fabsf(y0), fabsf(y1));
+  const float mag = fmaf(-qa * X, X, fmaf(fabsf(qb) * X, Y, -qc * Y * Y));
+  const float v = m + r1.y;  // log2 of the largest raw alpha
+  return !(v < -7.9943534f - fmaf(2e-5f, mag, 0.05f));
+}
+
 // ------------------------------------------------------------------ pass A
 template <int SC>
 __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
@@ -284,7 +328,8 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
       for (int j = 0; j + 1 < DI; ++j) qi[j] = qi[j + 1];
       qi[DI - 1] = ld_idx(pos + 32 * DI);
       if (*(volatile int*)&s_ndone == 4) break;  // every pixel finished
-      const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w);
+      const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w) &&
+                        tight_keep(r0, r1, pxlo, pxhi, g.ylo, g.yhi, A.wf, A.inv_w);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int ns = __popc(m);
       // azimuth wrap of the entry over the CTA: rint((pcx - mx) / w) is
