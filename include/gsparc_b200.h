@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define GSPARC_ABI_VERSION 4
+#define GSPARC_ABI_VERSION 5
 
 enum {
   GSPARC_OK = 0,
@@ -165,6 +165,11 @@ typedef struct gsparc_frame_layout {
                              (with_backward == 2; written by K3)          */
   int64_t off_sort_tmp;   /* u64  [pair_capacity] K3 scratch for tile lists
                              longer than shared memory                    */
+  int64_t off_ch_pos;     /* i32  [slots,32] list position (from the tile's
+                             start) of every chunk entry, written by the
+                             weights pass; the tensor-core raster backward
+                             walks only the entries a CTA used (f32
+                             frames with a backward; else 0)             */
 } gsparc_frame_layout;
 
 int gsparc_abi_version(void);

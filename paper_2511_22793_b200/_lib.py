@@ -12,7 +12,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsparc_b200.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 LOSS_STATS = 6  # GSPARC_LOSS_STATS
 
 OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
@@ -55,7 +55,8 @@ class CLayout(ctypes.Structure):
                  ("off_det_gcoef", c_i64), ("off_det_ggeo", c_i64),
                  ("off_stage", c_i64), ("off_seg", c_i64), ("seg_stride", c_i64),
                  ("off_pxw", c_i64), ("pxw_chunks", c_i64), ("off_ch_wm", c_i64),
-                 ("off_det_inv", c_i64), ("off_sort_tmp", c_i64)])
+                 ("off_det_inv", c_i64), ("off_sort_tmp", c_i64),
+                 ("off_ch_pos", c_i64)])
 
 
 class CEmitter(ctypes.Structure):

@@ -188,6 +188,7 @@ int gsparc_plan_frame(int64_t n, int32_t width, int32_t height, int64_t channels
   // segment never adds columns beyond ntx), so ntiles slots always suffice
   L.off_det_inv = det ? take(sizeof(int) * nn * (int64_t)L.ntiles) : 0;
   L.off_sort_tmp = take(8 * pair_capacity);
+  L.off_ch_pos = dtype == GSPARC_F32 && with_backward ? take(4 * 32 * L.ch_slots) : 0;
   L.total_bytes = o;
   *out = L;
   return GSPARC_OK;

@@ -39,6 +39,7 @@ namespace {
 constexpr int TC_NB = 32;           // entries per batch (GEMM N)
 constexpr int TC_KMAX = 64;         // channels (GEMM-1 K) supported
 constexpr int TC_NS = 4;            // coef / record stages (loader runs ahead)
+constexpr int K5_CCAP = 768;        // chunks per half tile for the compacted walk (else list walk)
 constexpr uint32_t TC_TMEM_COLS = 256;
 // TMEM columns: U hi [0,64) | U lo [64,128) | D1 x2 [128,192) | D2 x2 [192,256)
 constexpr uint32_t COL_UHI = 0, COL_ULO = 64, COL_D1 = 128, COL_D2 = 192;
@@ -59,6 +60,7 @@ struct TcShared {
   float4 fr[TC_NS][TC_NB][3];        // raster records per coef stage (+ conic, sigma)
   int idx[TC_NS][TC_NB];             // source index | bit 31: first copy of a seam duplicate
   float red[2][TC_NB][4][6];     // per scan warp geometric partial sums
+  int cs[K5_CCAP + 1];           // compacted walk: used entries before each chunk
   uint64_t coef_full[TC_NS], stage_empty[TC_NS], d1_full[2], d1_empty[2];
   uint64_t w_full[2], w_empty[2], d2_full[2], d2_empty[2], red_full[2], red_empty[2];
   uint32_t tmem;
@@ -204,6 +206,13 @@ struct BwdTcArgs {
   int w, h, ntx;
   int det;
   int lpt;  // longest-first CTA order
+  // compacted walk (non-deterministic frames): pass A's chunk entries of the
+  // half tile and their used bits
+  const uint32_t* ch_used;
+  const uint32_t* ch_idx;
+  const int* ch_pos;
+  const int* ch_n;
+  int compact;
 };
 
 __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
@@ -251,7 +260,69 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) nvisit = max(nvisit, A.wstop[tile * 8 + half * 4 + q]);
   if (nvisit == 0) return;
-  const int nbatch = (nvisit + TC_NB - 1) / TC_NB;
+  // Compacted walk (non-deterministic frames): only the entries that some
+  // pixel of this half tile included (pass A's ch_used bits, list order) can
+  // have a nonzero term -- an entry no pixel included has alpha under the cut
+  // or lies past every pixel's last included entry, so its scan terms, its
+  // weights (GEMM-2 column) and its gradients are all zero, and T / suffix
+  // pass it unchanged (rcp(1 - 0) = 1, fma(0, u, s) = s): skipping it is
+  // exact.  Batches are then 32 used entries; the deterministic mode keeps
+  // the list walk (its partial slots are indexed by list position).
+  int nwork = nvisit, cnch = 0;
+  int64_t cslot0 = 0;
+  bool cmp = false;
+  if (A.compact) {
+    cnch = A.ch_n[cta];
+    if (cnch <= K5_CCAP) {
+      cslot0 = 2 * (((int64_t)start + 31 * (int64_t)tile) >> 5) +
+               (int64_t)half * ((tile_end - start + 31) >> 5);
+      if (warp == 0) {
+        int run = 0;
+        for (int c0 = 0; c0 < cnch; c0 += 32) {
+          const int c = c0 + lane;
+          const int v = c < cnch ? __popc(__ldcg(A.ch_used + cslot0 + c)) : 0;
+          int inc = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+          }
+          if (c < cnch) S.cs[c] = run + inc - v;
+          run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) S.cs[cnch] = run;
+      }
+      __syncthreads();
+      nwork = S.cs[cnch];
+      cmp = true;
+      if (nwork == 0) return;
+    }
+  }
+  // e-th used entry of the half tile (list order): source index, and its
+  // list position from the tile's start in rel
+  auto centry = [&](int e, int& rel) -> int {
+    int lo = 0, hi = cnch;  // cs[lo] <= e < cs[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (S.cs[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    uint32_t m = __ldcg(A.ch_used + cslot0 + lo);
+    int r = e - S.cs[lo], k = 0;  // position of the r-th set bit of m
+#pragma unroll
+    for (int wdt = 16; wdt >= 1; wdt >>= 1) {
+      const int cnt = __popc(m & ((1u << wdt) - 1u));
+      if (r >= cnt) {
+        r -= cnt;
+        k += wdt;
+        m >>= wdt;
+      }
+    }
+    const int64_t o = (cslot0 + lo) * 32 + k;
+    rel = __ldcg(A.ch_pos + o);
+    return (int)__ldcg(A.ch_idx + o);
+  };
+  const int nbatch = (nwork + TC_NB - 1) / TC_NB;
   const int Cp = A.Cp;
   const uint32_t sbase = su32(sm);
 
@@ -345,7 +416,7 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   auto batch_range = [&](int b, int& b0, int& nb) {
-    const int bend = nvisit - TC_NB * b;
+    const int bend = nwork - TC_NB * b;
     b0 = bend > TC_NB ? bend - TC_NB : 0;
     nb = bend - b0;
   };
@@ -360,13 +431,16 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
       int idx = 0;
       bool dup = false;
       if (lane < nb) {
-        const int pos = start + b0 + lane;
-        idx = (int)(uint32_t)A.pairs[pos];
+        int rel = b0 + lane;  // list position from the tile's start
+        if (cmp) idx = centry(b0 + lane, rel);
+        const int pos = start + rel;
+        if (!cmp) idx = (int)(uint32_t)A.pairs[pos];
         dup = pos + 1 < tile_end && (int)(uint32_t)A.pairs[pos + 1] == idx;
         const float4 f0 = __ldg(A.rrec + 2 * (size_t)idx);
         const float4 f1 = __ldg(A.rrec + 2 * (size_t)idx + 1);
         S.fr[s][lane][0] = f0;
-        S.fr[s][lane][1] = f1;
+        // (xr, yr) are not used by the scan: z carries the list position
+        S.fr[s][lane][1] = make_float4(f1.x, f1.y, __int_as_float(rel), f1.w);
         // conic recovered from the pre-scaled exponent coefficients (K2) and
         // sigma = 2^(log2 sigma), once per entry instead of once per pixel
         const float k2 = (float)(-2.0 / LOG2E), k1 = (float)(-1.0 / LOG2E);
@@ -470,7 +544,9 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
       // before any wait
       int myidx = -1;
       if (lane < nb) {
-        const int pos = start + b0 + lane;
+        int rel = b0 + lane;
+        if (cmp) centry(b0 + lane, rel);
+        const int pos = start + rel;
         myidx = (int)(uint32_t)A.pairs[pos];
         if (pos + 1 < tile_end && (int)(uint32_t)A.pairs[pos + 1] == myidx)
           myidx |= (int)0x80000000;  // first copy of a seam duplicate
@@ -556,6 +632,7 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
         float ucg[8];
         tmem_ld8(d1row + 8 * g8, ucg);
         float dx[8], dy[8], e1[8], e2[8];
+        int rl[8];  // list positions (the loader's record z)
 #pragma unroll
         for (int t = 7; t >= 0; --t) {
           const int j = 8 * g8 + t;
@@ -567,6 +644,7 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
           const float qcy = f1.x * dy[t];
           e1[t] = fmaf(dx[t], tt, fmaf(qcy, dy[t], f1.y));  // q' + log2 sigma
           e2[t] = fmaf(dx[t], tt, qcy * dy[t]);             // q'
+          rl[t] = __float_as_int(f1.z);
         }
         float al[8], rom[8], ga[8];
         bool gon[8];
@@ -577,7 +655,7 @@ __global__ void __launch_bounds__(320, 1) k_raster_bwd_tc(BwdTcArgs A) {
           ga[t] = ex2_approx(e2[t]);
           // fast_alpha_full's alpha: min(raw, 0.99), zero below 1/255
           const float a = fminf(raw, ALPHA_MAX_F);
-          const bool on = (j < nb) & (b0 + j < lastp) & (a >= ALPHA_MIN_F);
+          const bool on = (j < nb) & (rl[t] < lastp) & (a >= ALPHA_MIN_F);
           al[t] = on ? a : 0.f;
           gon[t] = on & (raw < ALPHA_MAX_F);
         }
@@ -710,6 +788,13 @@ int launch_raster_bwd_tc(const gsparc_frame_layout& L, char* frame, int n_tx, in
       experiment_env("GSPARC_K5_LPT") ? atoi(experiment_env("GSPARC_K5_LPT")) : 1;
   A.lpt = lpt;
   A.det = det ? 1 : 0;
+  A.ch_used = (const uint32_t*)(frame + L.off_ch_used);
+  A.ch_idx = (const uint32_t*)(frame + L.off_ch_idx);
+  A.ch_pos = (const int*)(frame + L.off_ch_pos);
+  A.ch_n = (const int*)(frame + L.off_ch_n);
+  static const int cmp_env =
+      experiment_env("GSPARC_K5_COMPACT") ? atoi(experiment_env("GSPARC_K5_COMPACT")) : 1;
+  A.compact = !det && cmp_env && L.off_ch_pos != 0;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_raster_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TC);

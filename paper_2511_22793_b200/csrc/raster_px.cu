@@ -68,6 +68,7 @@ struct PxArgs {
   int64_t Cp, n;
   int C, w, h, ntx, ntiles;
   float t_eps, wf, inv_w;
+  int* ch_pos;  // [slots][32] list position of the entry (from the tile's start); null: not a backward frame
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         }
         const int64_t o = (slot0 + k) * PX_K + e;
         A.ch_idx[o] = idx;
+        if (A.ch_pos) A.ch_pos[o] = pos + lane;
         if (!SC && k >= A.wmax) {  // pass B recomputes these chunks' weights
           A.ch_rec[2 * o] = r0;
           A.ch_rec[2 * o + 1] = r1p;
@@ -1152,6 +1154,7 @@ static PxArgs make_px_args(const gsparc_frame_layout& L, char* frame, int n_tx, 
   A.ch_used = (uint32_t*)(frame + L.off_ch_used);
   A.dbg = nullptr;
   A.ch_idx = (uint32_t*)(frame + L.off_ch_idx);
+  A.ch_pos = L.off_ch_pos ? (int*)(frame + L.off_ch_pos) : nullptr;  // backward frames
   A.ch_rec = (float4*)(frame + L.off_ch_rec);
   A.ch_T = (float*)(frame + L.off_ch_T);
   A.ch_n = (int*)(frame + L.off_ch_n);

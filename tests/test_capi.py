@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version(L):
-    assert L.gsparc_abi_version() == 4
+    assert L.gsparc_abi_version() == 5
 
 
 def test_plan_frame_layout(L):
