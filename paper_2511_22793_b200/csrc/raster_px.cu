@@ -316,21 +316,8 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
     for (int j = 0; j < DI; ++j) qi[j] = ld_idx(32 * j);
 #pragma unroll
     for (int j = 0; j < DR; ++j) ld_rec(qi[j], qa[j], qb[j]);
-    for (int pos = 0; pos < end; pos += 32) {
-      const uint32_t idx = qi[0];
-      const float4 r0 = qa[0], r1 = qb[0];
-#pragma unroll
-      for (int j = 0; j + 1 < DR; ++j) {
-        qa[j] = qa[j + 1];
-        qb[j] = qb[j + 1];
-      }
-      ld_rec(qi[DR], qa[DR - 1], qb[DR - 1]);
-#pragma unroll
-      for (int j = 0; j + 1 < DI; ++j) qi[j] = qi[j + 1];
-      qi[DI - 1] = ld_idx(pos + 32 * DI);
-      if (*(volatile int*)&s_ndone == 4) break;  // every pixel finished
-      const bool keep = idx != 0xffffffffu && cull_keep(r0, r1, g, A.wf, A.inv_w) &&
-                        tight_keep(r0, r1, pxlo, pxhi, g.ylo, g.yhi, A.wf, A.inv_w);
+    // append one 32-entry batch (list positions p..p+31) to the ring
+    auto append = [&](uint32_t idx, float4 r0, float4 r1, bool keep, int p) {
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int ns = __popc(m);
       // azimuth wrap of the entry over the CTA: rint((pcx - mx) / w) is
@@ -352,7 +339,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         const int k = q < PX_K ? c : c + 1;
         const int e = q & (PX_K - 1);
         const float4 r1p =
-            make_float4(r1.x, r1.y, __int_as_float(pos + lane), __int_as_float((int)idx));
+            make_float4(r1.x, r1.y, __int_as_float(p + lane), __int_as_float((int)idx));
         s_ring[k % PX_RING][e][0] = r0;
         s_ring[k % PX_RING][e][1] = make_float4(r1.x, r1.y, r1p.z, -A.wf * k_lo);
         if (SC) {
@@ -362,7 +349,7 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         }
         const int64_t o = (slot0 + k) * PX_K + e;
         A.ch_idx[o] = idx;
-        if (A.ch_pos) A.ch_pos[o] = pos + lane;
+        if (A.ch_pos) A.ch_pos[o] = p + lane;
         if (!SC && k >= A.wmax) {  // pass B recomputes these chunks' weights
           A.ch_rec[2 * o] = r0;
           A.ch_rec[2 * o + 1] = r1p;
@@ -376,6 +363,32 @@ __global__ void __launch_bounds__(160) k_pxa(PxArgs A) {
         wrap_c = wrap_n;
         wrap_n = 0;
       }
+    };
+    // two batches per step: their culls are independent chains, so the
+    // producer warp -- alone on its scheduler and the limit of the CTAs
+    // whose pixels walk the whole list -- runs them side by side
+    for (int pos = 0; pos < end; pos += 64) {
+      const uint32_t idxA = qi[0], idxB = qi[1];
+      const float4 r0A = qa[0], r1A = qb[0], r0B = qa[1], r1B = qb[1];
+#pragma unroll
+      for (int j = 0; j + 2 < DR; ++j) {
+        qa[j] = qa[j + 2];
+        qb[j] = qb[j + 2];
+      }
+      ld_rec(qi[DR], qa[DR - 2], qb[DR - 2]);
+      ld_rec(qi[DR + 1], qa[DR - 1], qb[DR - 1]);
+#pragma unroll
+      for (int j = 0; j + 2 < DI; ++j) qi[j] = qi[j + 2];
+      qi[DI - 2] = ld_idx(pos + 32 * DI);
+      qi[DI - 1] = ld_idx(pos + 32 * (DI + 1));
+      if (*(volatile int*)&s_ndone == 4) break;  // every pixel finished
+      // (non-short-circuit: both tests of both batches issue branch-free)
+      const bool keepA = (idxA != 0xffffffffu) & cull_keep(r0A, r1A, g, A.wf, A.inv_w) &
+                         tight_keep(r0A, r1A, pxlo, pxhi, g.ylo, g.yhi, A.wf, A.inv_w);
+      const bool keepB = (idxB != 0xffffffffu) & cull_keep(r0B, r1B, g, A.wf, A.inv_w) &
+                         tight_keep(r0B, r1B, pxlo, pxhi, g.ylo, g.yhi, A.wf, A.inv_w);
+      append(idxA, r0A, r1A, keepA, pos);
+      if (pos + 32 < end) append(idxB, r0B, r1B, keepB, pos + 32);
     }
     if (fill > 0) {  // zero-opacity padding: alpha = 0, never included
       if (lane >= fill) {

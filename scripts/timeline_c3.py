@@ -76,3 +76,8 @@ cons = a0 + (da[:, 11] - da[:, 13]) / 1965.0
 tail = a1 - cons
 print("pass A consumers done -> CTA end (live-list append): max %.1f mean %.1f us; latest consumer end %.1f, latest CTA end %.1f"
       % (tail.max(), tail.mean(), cons.max(), a1.max()))
+# pass A roles of the last-finishing CTAs (cycles): producer waiting for a
+# free ring slot, consumers waiting for a filled one / walking
+print("pass A roles (cycles): cta tile.half nchunks prod_wait_empty prod_end | cons wait_full x4 | cons walk x4")
+for c in np.argsort(-a1)[:10]:
+    print(" ", c, "%d.%d" % (c >> 1, c & 1), da[c, 2], da[c, 0], da[c, 1], "|", da[c, 3:7], "|", da[c, 7:11])
