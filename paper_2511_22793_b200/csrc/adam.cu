@@ -83,14 +83,17 @@ __device__ __forceinline__ double adam_upd(double g, float& m, float& v, double 
 __global__ void k_adam(AdamArgs A, int64_t total, int geo_blocks) {
   // a frame whose pair buffer overflowed produced no valid gradient
   if (A.counters[GSPARC_CNT_NONFINITE] || A.counters[GSPARC_CNT_OVERFLOW]) return;
-  // step scalars (pow, exp/log/sin of the position schedule) once per CTA
+  // step scalars once per CTA: the two bias corrections on two threads, the
+  // position schedule (f64 exp/log/sin) on a third and only in the geometry
+  // blocks (the MLP blocks' CTAs start their loads sooner)
   __shared__ double s_sc[3];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 3) {
     const int64_t step = *A.step;
     const double t = (double)(step + 1);
-    s_sc[0] = 1.0 - pow(A.cfg.beta1, t);
-    s_sc[1] = 1.0 - pow(A.cfg.beta2, t);
-    s_sc[2] = position_lr_dev((double)step, A.cfg);
+    if (threadIdx.x == 0) s_sc[0] = 1.0 - pow(A.cfg.beta1, t);
+    if (threadIdx.x == 1) s_sc[1] = 1.0 - pow(A.cfg.beta2, t);
+    if (threadIdx.x == 2 && (int)blockIdx.x < geo_blocks)
+      s_sc[2] = position_lr_dev((double)step, A.cfg);
   }
   __syncthreads();
   const double b1 = A.cfg.beta1, b2 = A.cfg.beta2, eps = A.cfg.eps;
