@@ -8,7 +8,8 @@
 //   positions(n,3) | log_scales(n,3) | rotations(n,4) | raw_opacities(n) |
 //   mlp_weights(n,P)
 // (the ParamGradients groups of rasterizer.py:39-61), overwriting it.
-// Culled Gaussians get exact zeros.  TX batches sum their gradients.
+// Culled Gaussians, and on f32 frames those no pixel included, get exact
+// zeros.  TX batches sum their gradients.
 #include <type_traits>
 
 #include "common.cuh"
@@ -31,6 +32,10 @@ struct GBwdArgs {
   int64_t Cp;
   int P;
   int lane_tx;  // (5,16,C<=16) head: lane-per-TX MLP backward
+  // f32 frames: pass A's live flags (the Gaussian was included at some
+  // pixel); a Gaussian no pixel included has dL/dcoef = 0 for every TX and
+  // zero screen-space gradients, so every parameter gradient is exactly 0
+  const int* live;
 };
 
 constexpr int LANE_TX_JMAX = 12;  // flat MLP rows up to 384 parameters
@@ -65,7 +70,7 @@ __global__ void __launch_bounds__(128, 4) k_gauss_bwd(GBwdArgs A) {
   G* g_rot = g + 6 * n;
   G* g_op = g + 10 * n;
   G* g_w = g + 11 * n + i * (int64_t)P;
-  if (A.key[i] == ~0ULL) {
+  if (A.key[i] == ~0ULL || (A.live && !A.live[i])) {  // culled, or included nowhere
     if (lane < 3) put(g_pos, 3 * i + lane, 0.0);
     if (lane < 3) put(g_ls, 3 * i + lane, 0.0);
     if (lane < 4) put(g_rot, 4 * i + lane, 0.0);
@@ -292,7 +297,7 @@ template <typename FR, typename G>
 __global__ void __launch_bounds__(128) k_gauss_geo(GBwdArgs A) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.cloud.n) return;
-  if (A.key[i] == ~0ULL) return;  // culled: zeros written by k_gauss_bwd
+  if (A.key[i] == ~0ULL || (A.live && !A.live[i])) return;  // zeros written by k_gauss_bwd
   const int64_t n = A.cloud.n;
   G* g = (G*)A.grad;
   G* g_pos = g;
@@ -485,6 +490,7 @@ int launch_gauss_backward(const gsparc_cloud& cloud, const gsparc_view& view, co
   A.rec64 = (const double*)(frame + L.off_rec64);
   A.gcoef = frame + L.off_gcoef;
   A.ggeo = frame + L.off_ggeo;
+  A.live = L.dtype == GSPARC_F32 ? (const int*)(frame + L.off_live) : nullptr;
   A.grad = grad;
   A.Cp = L.channels;
   A.P = cloud.mlp_in * cloud.mlp_hidden + cloud.mlp_hidden + cloud.mlp_hidden * cloud.mlp_out +
