@@ -273,12 +273,14 @@ class Trainer:
         self.state = AdamState(self.dev)
         self.state.step_dev.fill_(int(start_step))
         self.step_no = int(start_step)
-        # size the pair buffer with one synchronous render
+        # size the pair buffer with one synchronous render.  The step renders
+        # with the lazy MLP: only Gaussians some pixel included need coef
+        # rows (pass B, K5's compacted walk); K6 recomputes the MLP itself
         self.tx.copy_(self.tx_all[:1].expand(self.Bl, 3))
         _, self.frame = self.R.forward(self.dev, pose, self.tx, self.w, self.h,
                                        image=self.img,
                                        with_backward=2 if cfg.deterministic else 1,
-                                       lazy=False)
+                                       lazy=True)
         self.graph = None
 
     def _gather(self):
@@ -287,7 +289,7 @@ class Trainer:
 
     def _compute(self):
         self.R.forward(self.dev, self.pose, self.tx, self.w, self.h,
-                       frame=self.frame, image=self.img, lazy=False,
+                       frame=self.frame, image=self.img, lazy=True,
                        sync_check=False)
         dimg, _ = self.loss.run(self.img, self.gt, self.sup,
                                 self.cfg.lambda_dssim)
